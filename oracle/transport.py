@@ -1,0 +1,82 @@
+"""FKS free transport as an exact integer shift per discrete velocity (oracle; tests only).
+
+P:243-257 (eq. f_bar): the piecewise-constant function of velocity v_k is advected exactly,
+f_bar_k^{*,n+1}(x) = f_bar_k^n(x - v_k dt); its discontinuities sit at x_{j+1/2} + n v_k dt
+(they are "remembered" off the grid).  Sampling at the cell centre x_j
+ therefore reads the piece whose origin cell is j + s^n_k with
+s^n_k = floor(1/2 - n v_k dt / dx) (the particle reinterpretation P:547-573 tracks
+only this one shift per velocity).  Storing the sampled values F^n_j = m[j + s^n] (an
+Eulerian array) the transport from step n to n+1 is the gather
+
+    f*_j[k] = F^n[j + delta_k][k],   delta_k = s^{n+1}_k - s^n_k  in {-1, 0, 1} at CFL <= 1.
+
+Reading #16: both sides compute c = (v * dt) / dx, t = n * c, floor(0.5 - t) in fp64, no FMA.
+Boundaries (reading #19): per face PERIODIC (wrap), GHOST (a fixed ghost vector, Dirichlet or
+inflow), OUTFLOW (clamp to the boundary cell).  When several axes leave the domain the
+lowest axis with a GHOST face wins; otherwise each axis is wrapped/clamped independently.
+Shift per spatial axis a uses velocity component a (x_i += v_i dt).
+Layout: F has shape spatial_shape + (N,)*dv; spatial_shape = (M_{dx-1}, .., M_0) (axis 0 fastest).
+"""
+import numpy as np
+
+from . import grid
+
+PERIODIC, GHOST, OUTFLOW = 0, 1, 2
+
+
+def shift_s(n, N, L, dt, dx):
+    """s^n_k = floor(0.5 - n * ((v_k * dt) / dx)) for the N nodes of one velocity axis."""
+    v = grid.nodes_1d(N, L)
+    c = (v * dt) / dx
+    t = np.float64(n) * c
+    return np.floor(0.5 - t).astype(np.int64)
+
+
+def shift_delta(n, N, L, dt, dx):
+    """delta_k = s^{n+1}_k - s^n_k."""
+    return shift_s(n + 1, N, L, dt, dx) - shift_s(n, N, L, dt, dx)
+
+
+def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None):
+    """f* from F^n.  bc: list of 2*dxdim face kinds [lo0, hi0, lo1, hi1, ...].
+    ghosts: dict face -> ghost vector of shape (N,)*dv."""
+    if dxdim == 0:
+        return F.copy()
+    sp_shape = F.shape[:dxdim]          # (M_{dx-1}, ..., M_0)
+    M = sp_shape[::-1]                  # M[a] = cells along space axis a
+    delta = shift_delta(n, N, L, dt, dx)
+    vshape = (N,) * dv
+    out = np.empty_like(F)
+    # velocity-axis index array per component a: component a is array axis dv-1-a
+    kcomp = np.meshgrid(*([np.arange(N)] * dv), indexing="ij")
+    kcomp = [kcomp[dv - 1 - a] for a in range(dv)]
+    jgrid = np.meshgrid(*[np.arange(m) for m in sp_shape], indexing="ij")
+    jgrid = [jgrid[dxdim - 1 - a] for a in range(dxdim)]  # jgrid[a]: index along space axis a
+    for jflat in range(int(np.prod(sp_shape))):
+        jidx = np.unravel_index(jflat, sp_shape)
+        j = [jidx[dxdim - 1 - a] for a in range(dxdim)]
+        src = []
+        ghost_face = np.full(vshape, -1, dtype=np.int64)
+        for a in range(dxdim):
+            s = j[a] + delta[kcomp[a]]
+            lo_out, hi_out = s < 0, s >= M[a]
+            for face, mask in ((2 * a, lo_out), (2 * a + 1, hi_out)):
+                kind = bc[face]
+                if kind == PERIODIC:
+                    s = np.where(mask, s % M[a], s)
+                elif kind == OUTFLOW:
+                    s = np.where(mask, np.clip(s, 0, M[a] - 1), s)
+                elif kind == GHOST:
+                    ghost_face = np.where(mask & (ghost_face < 0), face, ghost_face)
+                    s = np.where(mask, np.clip(s, 0, M[a] - 1), s)
+                else:
+                    raise ValueError(kind)
+            src.append(s)
+        idx = tuple(src[dxdim - 1 - b] for b in range(dxdim)) + tuple(
+            np.broadcast_to(g, vshape) for g in np.meshgrid(*([np.arange(N)] * dv), indexing="ij"))
+        vals = F[idx]
+        if ghosts is not None:
+            for face, gv in ghosts.items():
+                vals = np.where(ghost_face == face, gv, vals)
+        out[jidx] = vals
+    return out
