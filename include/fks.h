@@ -1,0 +1,148 @@
+/*
+ * fks.h -- C ABI of libfks, the B200-native hot path of the FKS + fast-spectral Boltzmann
+ * solver of Dimarco, Loubere, Narski and Rey (arXiv 1608.08009).
+ *
+ * Citation keys: P:n = PAPER.md line n (section / equation named beside it).
+ *
+ * What the library computes, per physical cell j and velocity node k:
+ *   a1  shift table     delta_k = s^{n+1}_k - s^n_k, s^n_k = floor(1/2 - n (v_k dt)/dx)
+ *                       (P:243-253 eq. f_bar; P:560-561 eq. transport)
+ *   a3  transport       f*_j[k] = F^n[j + delta_k][k] with periodic / ghost / outflow faces
+ *                       (sampling at x_j P:269-271)
+ *   a4-a7 collision     Q(f*) = fast spectral Carleman quadrature with A directions
+ *                       (P:390-452 eq. ode/FKM, 2D tables, 3D tables)
+ *   a8  projection      Pi Q = Q - Phi^T (Phi Phi^T)^{-1} Phi Q (P:319-358 eq. minim1)
+ *   a9  Euler           F^{n+1}_j = f*_j + (dt/tau) Pi Q_j  (P:273-275 eq. f_coll)
+ *   a10 moments         rho, u, T
+ *
+ * Conventions.
+ *  - Velocity lattice: N points per axis on [-L, L), cell-centred nodes
+ *    v_k = -L + (k + 1/2) 2L/N (reading #14).  n = N^dv.
+ *  - Layout of every distribution array: f[local_cell][k], fp64, k in C order over velocity
+ *    axes with v_x fastest (k = kx + N*ky + N*N*kz); cells in C order over the local grid
+ *    with space axis 0 fastest.
+ *  - Array pointers are DEVICE pointers owned by the caller unless the name says _host.
+ *    All device work is enqueued on the context stream (fks_set_stream; default stream 0)
+ *    and is asynchronous unless stated otherwise.  The library never frees caller memory.
+ *  - Errors: argument errors return FKS_E_INVAL / FKS_E_UNSUPPORTED synchronously with
+ *    nothing enqueued; CUDA launch/API failures return FKS_E_CUDA; a non-finite value
+ *    produced by fks_step sets a device flag that fks_check() reports as FKS_E_NONFINITE.
+ *    There is no CPU fallback: without a usable sm_100 device fks_init returns FKS_E_CUDA.
+ *  - A context is not thread-safe; use one per (process, device).
+ */
+#ifndef FKS_H
+#define FKS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fks_ctx fks_ctx;
+
+typedef enum {
+  FKS_OK = 0,
+  FKS_E_INVAL = -1,
+  FKS_E_UNSUPPORTED = -2,
+  FKS_E_NOMEM = -3,
+  FKS_E_CUDA = -4,
+  FKS_E_NCCL = -5,
+  FKS_E_NONFINITE = -6,
+  FKS_E_STATE = -7
+} fks_status;
+
+/* Face kinds (reading #19). */
+enum { FKS_BC_PERIODIC = 0, FKS_BC_GHOST = 1, FKS_BC_OUTFLOW = 2 };
+
+typedef struct {
+  int dv;          /* velocity dimension: 2 (Maxwell molecules) or 3 (hard spheres)          */
+  int dx;          /* space dimension 0..3; 0 = a batch of independent homogeneous cells    */
+  int64_t M[3];    /* local cells per space axis (axis 0 fastest); dx = 0: M[0] = batch size */
+  double h;        /* Delta x, equal on all axes                                    */
+  int bc[6];       /* face kinds [lo0, hi0, lo1, hi1, lo2, hi2] (ignored when dx = 0)       */
+} fks_grid;
+
+/* Create a context (P:85-91 model; P:141-158 kernels).
+ *   grid          physical grid (copied).
+ *   Nv            points per velocity axis: 8, 16 or 32 (the paper uses 8..64 per axis,
+ *                 P:624-625; 64 is NEXT work).
+ *   L             velocity box half-width (> 0).
+ *   M_dirs        number of quadrature directions A: dv = 2 -> theta_p = pi p / A, p = 1..A
+ *                 (P:490); dv = 3 -> 24 = the spherical 7-design (reading #17), a perfect
+ *                 square A1^2 = the (theta, phi) product grid of P:527-540 (reading #6);
+ *                 anything else needs fks_set_dirs.
+ *   kernel_gamma  VHS exponent alpha: must be 0 for dv = 2 and 1 for dv = 3, the
+ *                 two cases where Btilde is constant; otherwise FKS_E_UNSUPPORTED.
+ * Defaults: tau = 1, b0 = 1/(2 pi) (2D) or C1 = 1/(4 pi) (3D) (reading #7), R = 2 lambda pi
+ * (reading #1), projection on.  Builds the fp64 tables on the host and uploads them.
+ * Returns FKS_E_CUDA if no sm_100 device is present. */
+fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double kernel_gamma, fks_ctx** out);
+
+/* tau, kernel constant b0 / C1 (<= 0 keeps the default), scaled truncation radius R
+ * (<= 0 keeps the default), project (0/1).  Rebuilds the tables. */
+fks_status fks_set_params(fks_ctx* ctx, double tau, double kernel_const, double R, int project);
+
+/* Replace the direction set: e_host [M][dv] unit vectors, w_host [M] weights (host memory,
+ * copied).  For dv = 2 the perpendicular partner of e is e rotated by +pi/2. */
+fks_status fks_set_dirs(fks_ctx* ctx, const double* e_host, const double* w_host, int M);
+
+/* Ghost vector for a GHOST face (n values, device memory, copied into library memory). */
+fks_status fks_set_ghost(fks_ctx* ctx, int face, const double* ghost_f);
+
+/* Solid mask (host, one byte per local cell, copied): solid cells are not collided and keep
+ * their values (reading #19; specular reflection is NEXT work). NULL clears it. */
+fks_status fks_set_solid(fks_ctx* ctx, const uint8_t* solid_host);
+
+/* Stream (a cudaStream_t passed as void*) on which all later work is enqueued. */
+fks_status fks_set_stream(fks_ctx* ctx, void* cuda_stream);
+
+/* a4-a7: Q[cell][k] = Q(f[cell]) for every local cell, unprojected, user units, no 1/tau.
+ * f and Q must not overlap. */
+fks_status fks_collide(fks_ctx* ctx, const double* f, double* Q);
+
+/* a1 + a3: f_out = transported f_in for the step n -> n+1, then n += 1 (collision skipped).
+ * dt must equal the context dt once one was set (it is fixed per run, reading #15). */
+fks_status fks_transport(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
+
+/* a1..a9 fused: f_out = F^{n+1} from f_in = F^n, then n += 1.  f_out != f_in. */
+fks_status fks_step(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
+
+/* fks_step with HOST buffers: copies f_in_host to the device, steps, copies the result back
+ * to f_out_host and synchronises the stream (end-to-end path; pinned memory recommended). */
+fks_status fks_step_host(fks_ctx* ctx, const double* f_in_host, double* f_out_host, double dt);
+
+/* a10: rho[cell], u[cell][dv], T[cell] (T = int |v-u|^2 f / (dv rho), reading #12). */
+fks_status fks_moments(fks_ctx* ctx, const double* f, double* rho, double* u, double* T);
+
+/* Step counter n and time step dt (checkpoint / resume: shifts are pure functions of n). */
+fks_status fks_get_state(fks_ctx* ctx, int64_t* n, double* dt);
+fks_status fks_set_state(fks_ctx* ctx, int64_t n, double dt);
+
+/* Synchronise the stream; FKS_E_NONFINITE if any step produced a non-finite value since
+ * the last check (the flag is then cleared), FKS_E_CUDA on an asynchronous CUDA error. */
+fks_status fks_check(fks_ctx* ctx);
+
+/* Number of kernel launches the library has enqueued since the context was created. */
+int64_t fks_launch_count(const fks_ctx* ctx);
+
+fks_status fks_finalize(fks_ctx* ctx);
+const char* fks_strerror(fks_status s);
+
+/* ---- host-only introspection (no device needed; used by the CPU tests) ---------------- */
+
+/* The spectral tables exactly as uploaded, before folding (reading #10):
+ * alpha_host, alphap_host: [A][n] in FFT mode order (same layout as f), D_host: [n],
+ * w_host: [A], e_host: [A][dv].  Arrays may be NULL.  Returns the node-space factor
+ * s = Btilde kappa^{-(dv+gamma)} in *scale.  Arguments as in fks_init / fks_set_params. */
+fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, double kernel_const,
+                           double* alpha_host, double* alphap_host, double* D_host, double* w_host,
+                           double* e_host, double* scale);
+
+/* delta_k = s^{n+1}_k - s^n_k for the N nodes of one velocity axis (a1). */
+fks_status fks_host_shift(int64_t n, int Nv, double L, double dt, double h, int8_t* delta_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FKS_H */

@@ -1,0 +1,70 @@
+// Shared device-side definitions: kernel parameter blocks and the FKS transport gather.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fks {
+
+constexpr int kMaxN = 32;
+
+// a1 + a3: per-step shift table and boundary description.
+struct TransportParams {
+  int dx;                  // space dimension 0..3
+  int M[3];                // local cells per space axis (axis 0 fastest)
+  int bc[6];               // FKS_BC_* per face
+  int8_t delta[3][kMaxN];  // delta[a][k_a] = s^{n+1} - s^n for velocity component a
+  const double* ghost[6];  // ghost vectors (n values) of GHOST faces, device memory
+};
+
+struct StepParams {
+  const double* f_in;        // F^n       [cells][n]
+  double* f_out;             // F^{n+1} or Q [cells][n]
+  const double2* tables;     // folded tables, layout per kernel (see kernels*.cu)
+  double2* scratch;          // per-cluster exchange buffers (3D)
+  int* nonfinite;            // device flag
+  const int* cell_list;      // fluid cells to process (local linear indices)
+  int ncells;                // entries of cell_list
+  int A;                     // directions (tables hold A + 1 entries, the last is the loss)
+  int mode;                  // 0 = collide (write Q), 1 = step (project + Euler)
+  int project;               // apply a8
+  double dt_tau;             // dt / tau
+  double L, dv;              // velocity box half-width and spacing
+  double Ginv[25];           // (Phi Phi^T)^{-1}, (dv+2)^2 row-major
+  TransportParams tp;
+};
+
+// f*_cell[k]: the transported value for velocity k = (kx, ky, kz) (P:243-257 eq. f_bar sampled
+// at x_j).  Out-of-domain sources: PERIODIC wraps, OUTFLOW clamps, GHOST reads the
+// face's ghost vector (the lowest axis with a ghost face wins; reading #19).
+__device__ __forceinline__ double gather_fstar(const double* __restrict__ F, const TransportParams& tp,
+                                               int64_t cell, int k, int kx, int ky, int kz, int n) {
+  if (tp.dx == 0) return F[cell * n + k];
+  const int kc[3] = {kx, ky, kz};
+  int64_t rem = cell;
+  int64_t src = 0, stride = 1;
+  int gface = -1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a < tp.dx) {
+      const int Ma = tp.M[a];
+      const int j = (int)(rem % Ma);
+      rem /= Ma;
+      int s = j + tp.delta[a][kc[a]];
+      if (s < 0) {
+        if (tp.bc[2 * a] == 0) s += Ma;
+        else { if (tp.bc[2 * a] == 1 && gface < 0) gface = 2 * a; s = 0; }
+      } else if (s >= Ma) {
+        if (tp.bc[2 * a + 1] == 0) s -= Ma;
+        else { if (tp.bc[2 * a + 1] == 1 && gface < 0) gface = 2 * a + 1; s = Ma - 1; }
+      }
+      src += s * stride;
+      stride *= Ma;
+    }
+  }
+  if (gface >= 0) return tp.ghost[gface][k];
+  return F[src * n + k];
+}
+
+__device__ __forceinline__ double node_v(int k, double L, double dv) { return -L + (k + 0.5) * dv; }
+
+}  // namespace fks

@@ -1,0 +1,601 @@
+// libfks host side: the C ABI of include/fks.h, the fp64 table generator (written from the
+// paper independently of the oracle), the shift tables and the launch orchestration.
+// Compiled with -fmad=false / -ffp-contract=off for the host so the shift formula rounds
+// exactly as stated in DESIGN.md reading #16.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/fks.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+const double kLambda = 2.0 / (3.0 + std::sqrt(2.0));
+
+struct Dirs {
+  std::vector<double> e;  // [A][dv]
+  std::vector<double> w;  // [A]
+};
+
+// ------------------------------------------------------------------ radial functions
+double sinc(double x) { return x == 0.0 ? 1.0 : std::sin(x) / x; }
+// phi_R^2(s) = 2 R sinc(R s)
+double phi2(double s, double R) { return 2.0 * R * sinc(R * s); }
+// phi_R^3(s) = R^2 [2 sinc(R s) - sinc^2(R s / 2)]
+double phi3(double s, double R) {
+  const double h = sinc(0.5 * R * s);
+  return R * R * (2.0 * sinc(R * s) - h * h);
+}
+// Reading #2 (P:501-506 derivation): psi(s) = 2 pi R J1(R s) / s, psi(0) = pi R^2
+double psi3(double s, double R) { return s == 0.0 ? kPi * R * R : 2.0 * kPi * R * ::j1(R * s) / s; }
+
+// ------------------------------------------------------------------ direction sets
+Dirs dirs_2d(int A) {  // P:490 theta_p = pi p / A, weight pi / A (reading #5)
+  Dirs d;
+  for (int p = 1; p <= A; ++p) {
+    const double th = kPi * p / A;
+    d.e.push_back(std::cos(th));
+    d.e.push_back(std::sin(th));
+    d.w.push_back(kPi / A);
+  }
+  return d;
+}
+
+double cubic(double t) { return ((105.0 * t - 105.0) * t + 21.0) * t - 1.0; }
+
+// Reading #17: 24-point 7-design = O-orbit of (sqrt a, sqrt b, sqrt c), a<b<c the roots of
+// 105 t^3 - 105 t^2 + 21 t - 1 (bracketed by sign changes on [0,.1], [.1,.3], [.3,1]).
+Dirs dirs_design24() {
+  const double br[4] = {0.0, 0.1, 0.3, 1.0};
+  double r[3];
+  for (int i = 0; i < 3; ++i) {
+    double lo = br[i], hi = br[i + 1];
+    const bool up = cubic(lo) < 0.0;
+    for (int it = 0; it < 200; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if ((cubic(mid) < 0.0) == up) lo = mid; else hi = mid;
+    }
+    double t = 0.5 * (lo + hi);
+    for (int it = 0; it < 3; ++it) t -= cubic(t) / ((315.0 * t - 210.0) * t + 21.0);
+    r[i] = std::sqrt(t);
+  }
+  Dirs d;
+  int perm[3] = {0, 1, 2};
+  do {
+    const int inv = (perm[0] > perm[1]) + (perm[0] > perm[2]) + (perm[1] > perm[2]);
+    for (int sg = 0; sg < 8; ++sg) {
+      const double s0 = (sg & 4) ? -1.0 : 1.0, s1 = (sg & 2) ? -1.0 : 1.0, s2 = (sg & 1) ? -1.0 : 1.0;
+      const double det = ((inv & 1) ? -1.0 : 1.0) * s0 * s1 * s2;
+      if (det < 0) continue;
+      d.e.push_back(s0 * r[perm[0]]);
+      d.e.push_back(s1 * r[perm[1]]);
+      d.e.push_back(s2 * r[perm[2]]);
+      d.w.push_back(2.0 * kPi / 24.0);
+    }
+  } while (std::next_permutation(perm, perm + 3));
+  return d;
+}
+
+// P:527-540 with the sin(theta) Jacobian and midpoint theta (reading #6), sum w = 2 pi.
+Dirs dirs_product(int A1) {
+  Dirs d;
+  double tot = 0.0;
+  for (int p = 0; p < A1; ++p)
+    for (int q = 0; q < A1; ++q) {
+      const double th = (p + 0.5) * kPi / A1, ph = q * kPi / A1;
+      d.e.push_back(std::sin(th) * std::cos(ph));
+      d.e.push_back(std::sin(th) * std::sin(ph));
+      d.e.push_back(std::cos(th));
+      const double w = kPi * kPi * std::sin(th) / (A1 * A1);
+      d.w.push_back(w);
+      tot += w;
+    }
+  for (double& w : d.w) w *= 2.0 * kPi / tot;
+  return d;
+}
+
+bool default_dirs(int dv, int M, Dirs* out) {
+  if (M <= 0) return false;
+  if (dv == 2) { *out = dirs_2d(M); return true; }
+  if (M == 24) { *out = dirs_design24(); return true; }
+  const int a = (int)std::lround(std::sqrt((double)M));
+  if (a * a == M) { *out = dirs_product(a); return true; }
+  return false;
+}
+
+int mu(int j, int N) { return j < N / 2 ? j : j - N; }
+
+// Unfolded tables: alpha, alphap [A][n] in FFT mode order, symmetrised over
+// l -> -l (reading #10), and D = sum_p w_p alpha_p alpha'_p.
+void build_tables(int dv, int N, double R, const Dirs& dirs, std::vector<double>& alpha, std::vector<double>& alphap,
+                  std::vector<double>& D) {
+  const int A = (int)dirs.w.size();
+  const int n = dv == 3 ? N * N * N : N * N;
+  alpha.assign((size_t)A * n, 0.0);
+  alphap.assign((size_t)A * n, 0.0);
+  std::vector<double> ra(n), rb(n);
+  for (int p = 0; p < A; ++p) {
+    const double* e = &dirs.e[(size_t)p * dv];
+    for (int k = 0; k < n; ++k) {
+      const double lx = mu(k % N, N), ly = mu((k / N) % N, N), lz = dv == 3 ? mu(k / (N * N), N) : 0.0;
+      if (dv == 2) {
+        ra[k] = phi2(lx * e[0] + ly * e[1], R);
+        rb[k] = phi2(-lx * e[1] + ly * e[0], R);  // e_perp = e_{theta + pi/2}
+      } else {
+        const double dot = lx * e[0] + ly * e[1] + lz * e[2];
+        const double cx = ly * e[2] - lz * e[1], cy = lz * e[0] - lx * e[2], cz = lx * e[1] - ly * e[0];
+        ra[k] = phi3(dot, R);
+        rb[k] = psi3(std::sqrt(cx * cx + cy * cy + cz * cz), R);
+      }
+    }
+    for (int k = 0; k < n; ++k) {
+      const int x = k % N, y = (k / N) % N, z = dv == 3 ? k / (N * N) : 0;
+      const int mx = (N - x) % N, my = (N - y) % N, mz = (N - z) % N;
+      const int km = dv == 3 ? mx + N * (my + N * mz) : mx + N * my;
+      alpha[(size_t)p * n + k] = 0.5 * (ra[k] + ra[km]);
+      alphap[(size_t)p * n + k] = 0.5 * (rb[k] + rb[km]);
+    }
+  }
+  D.assign(n, 0.0);
+  for (int p = 0; p < A; ++p)
+    for (int k = 0; k < n; ++k) D[k] += dirs.w[p] * alpha[(size_t)p * n + k] * alphap[(size_t)p * n + k];
+}
+
+// s = Btilde kappa^-(d+gamma), Btilde = 2^{d-1} b (reading #3): 2D 2 b0 (L/pi)^2, 3D 4 C1 (L/pi)^4.
+double node_scale(int dv, double L, double kconst) {
+  const double k = L / kPi;
+  return dv == 2 ? 2.0 * kconst * k * k : 4.0 * kconst * k * k * k * k;
+}
+
+double default_kconst(int dv) { return dv == 2 ? 1.0 / (2.0 * kPi) : 1.0 / (4.0 * kPi); }
+
+// delta for one axis (a1, reading #16): s^n = floor(0.5 - n * ((v dt) / h)); no contraction.
+void shift_delta(int64_t n, int N, double L, double dt, double h, int8_t* out) {
+  const double dv = 2.0 * L / N;
+  for (int k = 0; k < N; ++k) {
+    volatile double v = -L + (k + 0.5) * dv;
+    volatile double vdt = v * dt;
+    volatile double c = vdt / h;
+    volatile double t0 = (double)n * c;
+    volatile double t1 = (double)(n + 1) * c;
+    volatile double a0 = 0.5 - t0;
+    volatile double a1 = 0.5 - t1;
+    out[k] = (int8_t)((int64_t)std::floor(a1) - (int64_t)std::floor(a0));
+  }
+}
+
+bool invert(std::vector<double> a, int m, double* out) {  // Gauss-Jordan with partial pivoting
+  std::vector<double> b((size_t)m * m, 0.0);
+  for (int i = 0; i < m; ++i) b[(size_t)i * m + i] = 1.0;
+  for (int c = 0; c < m; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < m; ++r)
+      if (std::fabs(a[(size_t)r * m + c]) > std::fabs(a[(size_t)piv * m + c])) piv = r;
+    if (a[(size_t)piv * m + c] == 0.0) return false;
+    for (int k = 0; k < m; ++k) {
+      std::swap(a[(size_t)c * m + k], a[(size_t)piv * m + k]);
+      std::swap(b[(size_t)c * m + k], b[(size_t)piv * m + k]);
+    }
+    const double d = a[(size_t)c * m + c];
+    for (int k = 0; k < m; ++k) { a[(size_t)c * m + k] /= d; b[(size_t)c * m + k] /= d; }
+    for (int r = 0; r < m; ++r) {
+      if (r == c) continue;
+      const double f = a[(size_t)r * m + c];
+      for (int k = 0; k < m; ++k) { a[(size_t)r * m + k] -= f * a[(size_t)c * m + k]; b[(size_t)r * m + k] -= f * b[(size_t)c * m + k]; }
+    }
+  }
+  std::memcpy(out, b.data(), sizeof(double) * m * m);
+  return true;
+}
+
+}  // namespace
+
+struct fks_ctx {
+  fks_grid grid;
+  int dv = 0, N = 0, n = 0, A = 0;
+  double L = 0, h = 0, gamma = 0;
+  double tau = 1.0, kconst = 0.0, R = 0.0;
+  int project = 1;
+  Dirs dirs;
+  int64_t ncells = 0;      // local cells
+  int64_t step_n = 0;      // FKS step counter n
+  double dt = 0.0;
+  cudaStream_t stream = 0;
+  int sm_count = 0;
+  int nclusters = 0;       // 3D persistent clusters
+  double Ginv[25];
+  double2* d_tables = nullptr;
+  double2* d_scratch = nullptr;
+  int* d_flag = nullptr;
+  int* d_fluid = nullptr;
+  int nfluid = 0;
+  int* d_solid_list = nullptr;
+  int nsolid = 0;
+  uint8_t* d_solid = nullptr;
+  double* d_ghost[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  double* d_host_in = nullptr;
+  double* d_host_out = nullptr;
+  int64_t launches = 0;
+};
+
+namespace {
+
+fks_status cuda_fail(cudaError_t e) { return e == cudaSuccess ? FKS_OK : FKS_E_CUDA; }
+
+fks_status upload_tables(fks_ctx* c) {
+  std::vector<double> al, alp, D;
+  build_tables(c->dv, c->N, c->R, c->dirs, al, alp, D);
+  const int n = c->n, N = c->N, A = c->A;
+  const double s = node_scale(c->dv, c->L, c->kconst);
+  std::vector<double2> T((size_t)(A + 1) * n);
+  // Fold s, w_p and 1/n (the kernels use the unnormalised forward DFT) into the tables.
+  for (int p = 0; p <= A; ++p)
+    for (int k = 0; k < n; ++k) {
+      const int x = k % N, y = (k / N) % N, z = c->dv == 3 ? k / (N * N) : 0;
+      // 3D layout T[p][l_y][l_z][l_x]; 2D layout T[p][l_y][l_x]
+      const size_t dst = c->dv == 3 ? (size_t)p * n + (size_t)y * N * N + (size_t)z * N + x : (size_t)p * n + k;
+      if (p < A)
+        T[dst] = make_double2(s * c->dirs.w[p] * al[(size_t)p * n + k] / n, alp[(size_t)p * n + k] / n);
+      else
+        T[dst] = make_double2(s * D[k] / n, 0.0);
+    }
+  if (c->d_tables) cudaFree(c->d_tables);
+  c->d_tables = nullptr;
+  if (cudaMalloc(&c->d_tables, T.size() * sizeof(double2)) != cudaSuccess) return FKS_E_NOMEM;
+  return cuda_fail(cudaMemcpy(c->d_tables, T.data(), T.size() * sizeof(double2), cudaMemcpyHostToDevice));
+}
+
+void build_gram(fks_ctx* c) {
+  const int m = c->dv + 2;
+  std::vector<double> g((size_t)m * m, 0.0);
+  const double dv = 2.0 * c->L / c->N;
+  for (int k = 0; k < c->n; ++k) {
+    double v[3] = {-c->L + (k % c->N + 0.5) * dv, -c->L + ((k / c->N) % c->N + 0.5) * dv,
+                   c->dv == 3 ? -c->L + (k / (c->N * c->N) + 0.5) * dv : 0.0};
+    double phi[5];
+    phi[0] = 1.0;
+    double v2 = 0.0;
+    for (int a = 0; a < c->dv; ++a) { phi[1 + a] = v[a]; v2 += v[a] * v[a]; }
+    phi[m - 1] = v2;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) g[(size_t)i * m + j] += phi[i] * phi[j];
+  }
+  std::memset(c->Ginv, 0, sizeof(c->Ginv));
+  invert(g, m, c->Ginv);
+}
+
+fks_status set_cell_lists(fks_ctx* c, const uint8_t* solid_host) {
+  std::vector<int> fluid, solid;
+  for (int64_t i = 0; i < c->ncells; ++i) {
+    if (solid_host && solid_host[i]) solid.push_back((int)i); else fluid.push_back((int)i);
+  }
+  cudaFree(c->d_fluid); cudaFree(c->d_solid_list); cudaFree(c->d_solid);
+  c->d_fluid = nullptr; c->d_solid_list = nullptr; c->d_solid = nullptr;
+  c->nfluid = (int)fluid.size();
+  c->nsolid = (int)solid.size();
+  if (!fluid.empty()) {
+    if (cudaMalloc(&c->d_fluid, fluid.size() * sizeof(int)) != cudaSuccess) return FKS_E_NOMEM;
+    cudaMemcpy(c->d_fluid, fluid.data(), fluid.size() * sizeof(int), cudaMemcpyHostToDevice);
+  }
+  if (!solid.empty()) {
+    if (cudaMalloc(&c->d_solid_list, solid.size() * sizeof(int)) != cudaSuccess) return FKS_E_NOMEM;
+    cudaMemcpy(c->d_solid_list, solid.data(), solid.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (cudaMalloc(&c->d_solid, c->ncells) != cudaSuccess) return FKS_E_NOMEM;
+    cudaMemcpy(c->d_solid, solid_host, c->ncells, cudaMemcpyHostToDevice);
+  }
+  return cuda_fail(cudaGetLastError());
+}
+
+void fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift) {
+  std::memset(tp, 0, sizeof(*tp));
+  tp->dx = with_shift ? c->grid.dx : 0;
+  for (int a = 0; a < 3; ++a) tp->M[a] = (int)c->grid.M[a];
+  for (int f = 0; f < 6; ++f) { tp->bc[f] = c->grid.bc[f]; tp->ghost[f] = c->d_ghost[f]; }
+  if (with_shift)
+    for (int a = 0; a < c->grid.dx; ++a) shift_delta(c->step_n, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
+}
+
+fks::StepParams base_params(fks_ctx* c, const double* f_in, double* f_out, int mode) {
+  fks::StepParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.f_in = f_in;
+  p.f_out = f_out;
+  p.tables = c->d_tables;
+  p.scratch = c->d_scratch;
+  p.nonfinite = c->d_flag;
+  p.A = c->A;
+  p.mode = mode;
+  p.project = c->project;
+  p.dt_tau = c->dt / c->tau;
+  p.L = c->L;
+  p.dv = 2.0 * c->L / c->N;
+  std::memcpy(p.Ginv, c->Ginv, sizeof(p.Ginv));
+  return p;
+}
+
+fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
+  if (p.ncells == 0) return FKS_OK;
+  cudaError_t e;
+  if (c->dv == 3) {
+    const int ncl = std::min<int64_t>(p.ncells, c->nclusters);
+    e = fks::launch_step3d(c->N, p, ncl, c->stream);
+  } else {
+    const int per = fks::cells_per_block2d(c->N);
+    const int64_t need = (p.ncells + per - 1) / per;
+    const int nb = (int)std::min<int64_t>(need, (int64_t)c->sm_count);
+    e = fks::launch_step2d(c->N, p, nb, c->stream);
+  }
+  c->launches++;
+  return cuda_fail(e);
+}
+
+bool valid_N(int N) { return N == 8 || N == 16 || N == 32; }
+
+}  // namespace
+
+extern "C" {
+
+const char* fks_strerror(fks_status s) {
+  switch (s) {
+    case FKS_OK: return "ok";
+    case FKS_E_INVAL: return "invalid argument";
+    case FKS_E_UNSUPPORTED: return "unsupported configuration";
+    case FKS_E_NOMEM: return "out of device memory";
+    case FKS_E_CUDA: return "CUDA error (no sm_100 device, launch failure or asynchronous fault)";
+    case FKS_E_NCCL: return "NCCL error";
+    case FKS_E_NONFINITE: return "non-finite value produced by a step";
+    case FKS_E_STATE: return "invalid state (dt changed mid-run or call out of order)";
+  }
+  return "unknown status";
+}
+
+fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, double kernel_const, double* alpha_host,
+                           double* alphap_host, double* D_host, double* w_host, double* e_host, double* scale) {
+  if ((dv != 2 && dv != 3) || !valid_N(Nv) || !(L > 0)) return FKS_E_INVAL;
+  Dirs d;
+  if (!default_dirs(dv, M_dirs, &d)) return FKS_E_UNSUPPORTED;
+  if (!(R > 0)) R = 2.0 * kLambda * kPi;
+  if (!(kernel_const > 0)) kernel_const = default_kconst(dv);
+  std::vector<double> al, alp, D;
+  build_tables(dv, Nv, R, d, al, alp, D);
+  if (alpha_host) std::memcpy(alpha_host, al.data(), al.size() * sizeof(double));
+  if (alphap_host) std::memcpy(alphap_host, alp.data(), alp.size() * sizeof(double));
+  if (D_host) std::memcpy(D_host, D.data(), D.size() * sizeof(double));
+  if (w_host) std::memcpy(w_host, d.w.data(), d.w.size() * sizeof(double));
+  if (e_host) std::memcpy(e_host, d.e.data(), d.e.size() * sizeof(double));
+  if (scale) *scale = node_scale(dv, L, kernel_const);
+  return FKS_OK;
+}
+
+fks_status fks_host_shift(int64_t n, int Nv, double L, double dt, double h, int8_t* delta_host) {
+  if (Nv <= 0 || Nv > fks::kMaxN || !(L > 0) || !(h > 0) || !delta_host || n < 0) return FKS_E_INVAL;
+  shift_delta(n, Nv, L, dt, h, delta_host);
+  return FKS_OK;
+}
+
+fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double kernel_gamma, fks_ctx** out) {
+  if (!grid || !out) return FKS_E_INVAL;
+  *out = nullptr;
+  const int dv = grid->dv;
+  if ((dv != 2 && dv != 3) || !valid_N(Nv) || !(L > 0) || grid->dx < 0 || grid->dx > 3 || grid->dx > dv)
+    return FKS_E_INVAL;
+  if ((dv == 2 && kernel_gamma != 0.0) || (dv == 3 && kernel_gamma != 1.0)) return FKS_E_UNSUPPORTED;
+  int64_t ncells = 1;
+  const int axes = grid->dx == 0 ? 1 : grid->dx;
+  for (int a = 0; a < axes; ++a) {
+    if (grid->M[a] <= 0) return FKS_E_INVAL;
+    ncells *= grid->M[a];
+  }
+  if (ncells > INT32_MAX) return FKS_E_INVAL;
+  if (grid->dx > 0 && !(grid->h > 0)) return FKS_E_INVAL;
+  for (int f = 0; f < 2 * grid->dx; ++f)
+    if (grid->bc[f] < 0 || grid->bc[f] > 2) return FKS_E_INVAL;
+  Dirs dirs;
+  if (!default_dirs(dv, M_dirs, &dirs)) return FKS_E_UNSUPPORTED;
+
+  int dev = 0;
+  cudaDeviceProp prop;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return FKS_E_CUDA;
+  if (prop.major != 10) return FKS_E_CUDA;  // built for sm_100a only
+
+  fks_ctx* c = new (std::nothrow) fks_ctx();
+  if (!c) return FKS_E_NOMEM;
+  c->grid = *grid;
+  if (grid->dx == 0) {
+    c->grid.M[1] = c->grid.M[2] = 1;
+  } else {
+    for (int a = grid->dx; a < 3; ++a) c->grid.M[a] = 1;
+  }
+  c->dv = dv;
+  c->N = Nv;
+  c->n = dv == 3 ? Nv * Nv * Nv : Nv * Nv;
+  c->L = L;
+  c->h = grid->h;
+  c->gamma = kernel_gamma;
+  c->kconst = default_kconst(dv);
+  c->R = 2.0 * kLambda * kPi;
+  c->dirs = dirs;
+  c->A = (int)dirs.w.size();
+  c->ncells = ncells;
+  c->sm_count = prop.multiProcessorCount;
+  fks_status st = upload_tables(c);
+  if (st == FKS_OK) {
+    build_gram(c);
+    if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess) st = FKS_E_NOMEM;
+    else cudaMemset(c->d_flag, 0, sizeof(int));
+  }
+  if (st == FKS_OK && dv == 3) {
+    c->nclusters = fks::max_active_clusters3d(Nv);
+    if (c->nclusters <= 0) st = FKS_E_CUDA;
+    else if (cudaMalloc(&c->d_scratch, (size_t)c->nclusters * fks::scratch_elems3d(Nv) * sizeof(double2)) != cudaSuccess)
+      st = FKS_E_NOMEM;
+  }
+  if (st == FKS_OK) st = set_cell_lists(c, nullptr);
+  if (st != FKS_OK) { fks_finalize(c); return st; }
+  *out = c;
+  return FKS_OK;
+}
+
+fks_status fks_set_params(fks_ctx* c, double tau, double kernel_const, double R, int project) {
+  if (!c || !(tau > 0)) return FKS_E_INVAL;
+  c->tau = tau;
+  if (kernel_const > 0) c->kconst = kernel_const;
+  if (R > 0) c->R = R;
+  c->project = project ? 1 : 0;
+  return upload_tables(c);
+}
+
+fks_status fks_set_dirs(fks_ctx* c, const double* e_host, const double* w_host, int M) {
+  if (!c || !e_host || !w_host || M <= 0) return FKS_E_INVAL;
+  Dirs d;
+  d.e.assign(e_host, e_host + (size_t)M * c->dv);
+  d.w.assign(w_host, w_host + M);
+  c->dirs = d;
+  c->A = M;
+  return upload_tables(c);
+}
+
+fks_status fks_set_ghost(fks_ctx* c, int face, const double* ghost_f) {
+  if (!c || face < 0 || face >= 6 || !ghost_f) return FKS_E_INVAL;
+  if (!c->d_ghost[face] && cudaMalloc(&c->d_ghost[face], (size_t)c->n * sizeof(double)) != cudaSuccess)
+    return FKS_E_NOMEM;
+  return cuda_fail(cudaMemcpyAsync(c->d_ghost[face], ghost_f, (size_t)c->n * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   c->stream));
+}
+
+fks_status fks_set_solid(fks_ctx* c, const uint8_t* solid_host) {
+  if (!c) return FKS_E_INVAL;
+  return set_cell_lists(c, solid_host);
+}
+
+fks_status fks_set_stream(fks_ctx* c, void* s) {
+  if (!c) return FKS_E_INVAL;
+  c->stream = (cudaStream_t)s;
+  return FKS_OK;
+}
+
+fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
+  if (!c || !f || !Q || f == Q) return FKS_E_INVAL;
+  fks::StepParams p = base_params(c, f, Q, 0);
+  fill_transport(c, &p.tp, false);
+  p.cell_list = nullptr;
+  p.ncells = (int)c->ncells;
+  return run_collision(c, p);
+}
+
+static fks_status check_dt(fks_ctx* c, double dt) {
+  if (!(dt > 0)) return FKS_E_INVAL;
+  for (int f = 0; f < 2 * c->grid.dx; ++f)
+    if (c->grid.bc[f] == FKS_BC_GHOST && !c->d_ghost[f]) return FKS_E_STATE;
+  if (c->dt == 0.0) c->dt = dt;
+  else if (c->dt != dt) return FKS_E_STATE;
+  return FKS_OK;
+}
+
+fks_status fks_transport(fks_ctx* c, const double* f_in, double* f_out, double dt) {
+  if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
+  fks_status st = check_dt(c, dt);
+  if (st != FKS_OK) return st;
+  fks::TransportParams tp;
+  fill_transport(c, &tp, true);
+  cudaError_t e = fks::launch_transport(f_in, f_out, tp, c->d_solid, c->ncells, c->n, c->N, c->dv, c->stream);
+  c->launches++;
+  if (e != cudaSuccess) return FKS_E_CUDA;
+  c->step_n++;
+  return FKS_OK;
+}
+
+fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
+  if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
+  fks_status st = check_dt(c, dt);
+  if (st != FKS_OK) return st;
+  if (c->nsolid) {
+    if (fks::launch_copy_cells(f_in, f_out, c->d_solid_list, c->nsolid, c->n, c->stream) != cudaSuccess)
+      return FKS_E_CUDA;
+    c->launches++;
+  }
+  fks::StepParams p = base_params(c, f_in, f_out, 1);
+  fill_transport(c, &p.tp, true);
+  p.cell_list = c->d_fluid;
+  p.ncells = c->nfluid;
+  st = run_collision(c, p);
+  if (st != FKS_OK) return st;
+  c->step_n++;
+  return FKS_OK;
+}
+
+fks_status fks_step_host(fks_ctx* c, const double* f_in_host, double* f_out_host, double dt) {
+  if (!c || !f_in_host || !f_out_host) return FKS_E_INVAL;
+  const size_t bytes = (size_t)c->ncells * c->n * sizeof(double);
+  if (!c->d_host_in) {
+    if (cudaMalloc(&c->d_host_in, bytes) != cudaSuccess) return FKS_E_NOMEM;
+    if (cudaMalloc(&c->d_host_out, bytes) != cudaSuccess) return FKS_E_NOMEM;
+  }
+  if (cudaMemcpyAsync(c->d_host_in, f_in_host, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    return FKS_E_CUDA;
+  fks_status st = fks_step(c, c->d_host_in, c->d_host_out, dt);
+  if (st != FKS_OK) return st;
+  if (cudaMemcpyAsync(f_out_host, c->d_host_out, bytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    return FKS_E_CUDA;
+  return cuda_fail(cudaStreamSynchronize(c->stream));
+}
+
+fks_status fks_moments(fks_ctx* c, const double* f, double* rho, double* u, double* T) {
+  if (!c || !f || !rho || !u || !T) return FKS_E_INVAL;
+  cudaError_t e = fks::launch_moments(f, rho, u, T, c->ncells, c->N, c->dv, c->L, 2.0 * c->L / c->N, c->stream);
+  c->launches++;
+  return cuda_fail(e);
+}
+
+fks_status fks_get_state(fks_ctx* c, int64_t* n, double* dt) {
+  if (!c) return FKS_E_INVAL;
+  if (n) *n = c->step_n;
+  if (dt) *dt = c->dt;
+  return FKS_OK;
+}
+
+fks_status fks_set_state(fks_ctx* c, int64_t n, double dt) {
+  if (!c || n < 0 || dt < 0) return FKS_E_INVAL;
+  c->step_n = n;
+  c->dt = dt;
+  return FKS_OK;
+}
+
+fks_status fks_check(fks_ctx* c) {
+  if (!c) return FKS_E_INVAL;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return FKS_E_CUDA;
+  int flag = 0;
+  if (cudaMemcpy(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return FKS_E_CUDA;
+  if (flag) {
+    cudaMemset(c->d_flag, 0, sizeof(int));
+    return FKS_E_NONFINITE;
+  }
+  return FKS_OK;
+}
+
+int64_t fks_launch_count(const fks_ctx* c) { return c ? c->launches : -1; }
+
+fks_status fks_finalize(fks_ctx* c) {
+  if (!c) return FKS_E_INVAL;
+  cudaFree(c->d_tables);
+  cudaFree(c->d_scratch);
+  cudaFree(c->d_flag);
+  cudaFree(c->d_fluid);
+  cudaFree(c->d_solid_list);
+  cudaFree(c->d_solid);
+  for (auto& g : c->d_ghost) cudaFree(g);
+  cudaFree(c->d_host_in);
+  cudaFree(c->d_host_out);
+  delete c;
+  return FKS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,29 @@
+// Launchers of the device kernels (host-callable, used by fks_api.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace fks {
+
+// 3D (hard spheres): cluster of 8 CTAs per cell; scratch = nclusters * scratch_elems3d(N) double2.
+cudaError_t launch_step3d(int N, const StepParams& p, int nclusters, cudaStream_t s);
+int max_active_clusters3d(int N);
+size_t scratch_elems3d(int N);
+
+// 2D (Maxwell molecules): cells_per_block2d(N) cells per CTA.
+cudaError_t launch_step2d(int N, const StepParams& p, int nblocks, cudaStream_t s);
+int cells_per_block2d(int N);
+
+// a1 + a3 only: f_out[c] = f*[c] for all local cells (solid cells copied unchanged).
+cudaError_t launch_transport(const double* f_in, double* f_out, const TransportParams& tp, const uint8_t* solid,
+                             int64_t ncells, int n, int N, int dv, cudaStream_t s);
+
+// Copy the listed cells f_out[c] = f_in[c] (solid cells in fks_step).
+cudaError_t launch_copy_cells(const double* f_in, double* f_out, const int* cells, int count, int n, cudaStream_t s);
+
+// a10: rho, u[dv], T per cell.
+cudaError_t launch_moments(const double* f, double* rho, double* u, double* T, int64_t ncells, int N, int dv,
+                           double L, double dv_spacing, cudaStream_t s);
+
+}  // namespace fks

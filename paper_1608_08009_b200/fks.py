@@ -1,0 +1,161 @@
+"""Thin Python binding of the libfks C ABI (include/fks.h): same names, argument marshalling only.
+
+Device arrays are torch float64 CUDA tensors (plumbing: device memory and streams); every
+step of the hot path runs in the library's kernels.  No function here computes any part of
+the method, and nothing falls back to the CPU.
+"""
+import ctypes
+
+import numpy as np
+
+from ._lib import FksError, FksGrid, check, load  # noqa: F401
+
+BC_PERIODIC, BC_GHOST, BC_OUTFLOW = 0, 1, 2
+
+
+def _ptr(t):
+    """Device pointer of a contiguous float64 CUDA tensor."""
+    if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class Context:
+    """Owns one fks_ctx* (fks_init ... fks_finalize)."""
+
+    def __init__(self, dv, dx, M, Nv, L, M_dirs, kernel_gamma=None, h=1.0, bc=None):
+        lib = load()
+        g = FksGrid()
+        g.dv, g.dx = dv, dx
+        Ms = list(M) + [1] * (3 - len(M))
+        for a in range(3):
+            g.M[a] = int(Ms[a])
+        g.h = float(h)
+        bc = list(bc or []) + [0] * (6 - len(bc or []))
+        for f in range(6):
+            g.bc[f] = int(bc[f])
+        if kernel_gamma is None:
+            kernel_gamma = 0.0 if dv == 2 else 1.0
+        h_ = ctypes.c_void_p()
+        check(lib.fks_init(ctypes.byref(g), Nv, float(L), M_dirs, float(kernel_gamma), ctypes.byref(h_)), "fks_init")
+        self._lib, self.handle = lib, h_
+        self.dv, self.dx, self.N, self.L = dv, dx, Nv, L
+        self.n = Nv ** dv
+        self.ncells = int(np.prod([int(m) for m in (M if dx else M[:1])]))
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.fks_finalize(self.handle)
+            self.handle = None
+
+    # ---- configuration -------------------------------------------------------------------
+    def set_params(self, tau=1.0, kernel_const=0.0, R=0.0, project=True):
+        check(self._lib.fks_set_params(self.handle, float(tau), float(kernel_const), float(R), int(project)),
+              "fks_set_params")
+
+    def set_dirs(self, e, w):
+        e = np.ascontiguousarray(e, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        check(self._lib.fks_set_dirs(self.handle, _dptr(e), _dptr(w), len(w)), "fks_set_dirs")
+
+    def set_ghost(self, face, ghost):
+        check(self._lib.fks_set_ghost(self.handle, face, _ptr(ghost)), "fks_set_ghost")
+
+    def set_solid(self, mask):
+        if mask is None:
+            check(self._lib.fks_set_solid(self.handle, None), "fks_set_solid")
+            return
+        m = np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+        check(self._lib.fks_set_solid(self.handle, m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))), "fks_set_solid")
+
+    def set_stream(self, stream):
+        """stream: a torch.cuda.Stream (or None for the default stream)."""
+        check(self._lib.fks_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream if stream else 0)),
+              "fks_set_stream")
+
+    # ---- hot path ------------------------------------------------------------------------
+    def collide(self, f, Q):
+        check(self._lib.fks_collide(self.handle, _ptr(f), _ptr(Q)), "fks_collide")
+
+    def transport(self, f_in, f_out, dt):
+        check(self._lib.fks_transport(self.handle, _ptr(f_in), _ptr(f_out), float(dt)), "fks_transport")
+
+    def step(self, f_in, f_out, dt):
+        check(self._lib.fks_step(self.handle, _ptr(f_in), _ptr(f_out), float(dt)), "fks_step")
+
+    def step_host(self, f_in, f_out, dt):
+        """f_in, f_out: host float64 arrays/tensors (pinned recommended); synchronous."""
+        pi = ctypes.c_void_p(f_in.data_ptr() if hasattr(f_in, "data_ptr") else f_in.ctypes.data)
+        po = ctypes.c_void_p(f_out.data_ptr() if hasattr(f_out, "data_ptr") else f_out.ctypes.data)
+        check(self._lib.fks_step_host(self.handle, pi, po, float(dt)), "fks_step_host")
+
+    def moments(self, f, rho, u, T):
+        check(self._lib.fks_moments(self.handle, _ptr(f), _ptr(rho), _ptr(u), _ptr(T)), "fks_moments")
+
+    # ---- state ---------------------------------------------------------------------------
+    def get_state(self):
+        n, dt = ctypes.c_int64(), ctypes.c_double()
+        check(self._lib.fks_get_state(self.handle, ctypes.byref(n), ctypes.byref(dt)), "fks_get_state")
+        return n.value, dt.value
+
+    def set_state(self, n, dt):
+        check(self._lib.fks_set_state(self.handle, int(n), float(dt)), "fks_set_state")
+
+    def check(self):
+        check(self._lib.fks_check(self.handle), "fks_check")
+
+    def launch_count(self):
+        return int(self._lib.fks_launch_count(self.handle))
+
+
+# ---- function-style aliases with the C names ---------------------------------------------
+def fks_init(dv, dx, M, Nv, L, M_dirs, kernel_gamma=None, h=1.0, bc=None):
+    return Context(dv, dx, M, Nv, L, M_dirs, kernel_gamma, h, bc)
+
+
+def fks_collide(ctx, f, Q):
+    ctx.collide(f, Q)
+
+
+def fks_transport(ctx, f_in, f_out, dt):
+    ctx.transport(f_in, f_out, dt)
+
+
+def fks_step(ctx, f_in, f_out, dt):
+    ctx.step(f_in, f_out, dt)
+
+
+def fks_moments(ctx, f, rho, u, T):
+    ctx.moments(f, rho, u, T)
+
+
+def fks_finalize(ctx):
+    ctx.close()
+
+
+def host_tables(dv, Nv, L, M_dirs, R=0.0, kernel_const=0.0):
+    """fks_host_tables: (alpha [A, n], alphap [A, n], D [n], w [A], e [A, dv], scale)."""
+    lib = load()
+    A = M_dirs
+    n = Nv ** dv
+    al, alp = np.zeros((A, n)), np.zeros((A, n))
+    D, w, e = np.zeros(n), np.zeros(A), np.zeros((A, dv))
+    s = ctypes.c_double()
+    check(lib.fks_host_tables(dv, Nv, float(L), M_dirs, float(R), float(kernel_const), _dptr(al), _dptr(alp),
+                              _dptr(D), _dptr(w), _dptr(e), ctypes.byref(s)), "fks_host_tables")
+    return al, alp, D, w, e, s.value
+
+
+def host_shift(n, Nv, L, dt, h):
+    """fks_host_shift: delta_k (int8 [Nv])."""
+    out = np.zeros(Nv, dtype=np.int8)
+    check(load().fks_host_shift(int(n), Nv, float(L), float(dt), float(h),
+                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_int8))), "fks_host_shift")
+    return out

@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Criteria:
+  Q from fks_collide:   per cell max_k |Q_gpu - Q_orc| / max_k (|Q+_orc| + |Q-_orc|) <= 1e-11
+  F^{n+1} from fks_step: per cell max_k |f_gpu - f_orc| / max_k |f_orc|             <= 1e-11
+  transport:            bitwise; moments: 1e-13 relative.
+The oracle evaluator is `collide_direct` (the literal O(n^2) bilinear form) wherever it finishes
+in seconds and `collide_fft` (pinned to it, tests/test_oracle_pins.py P4) elsewhere.
+"""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import collision, grid, moments, projection, step as ostep, tables, transport
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+    if not _t.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    return _t
+
+
+@pytest.fixture(scope="module")
+def fks():
+    from paper_1608_08009_b200 import fks as _f
+    return _f
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel_err_Q(Qg, f, tab, direct):
+    """Per-cell parity norm of §8(c.5)."""
+    worst = 0.0
+    for c in range(f.shape[0]):
+        ev = collision.collide_direct if direct else collision.collide_fft
+        Q, g, l = ev(f[c], tab, return_parts=True)
+        worst = max(worst, np.max(np.abs(Qg[c] - Q)) / np.max(np.abs(g) + np.abs(l)))
+    return worst
+
+
+# ---------------------------------------------------------------- a4-a7: collide
+@pytest.mark.parametrize("N,L", [(8, 4.0), (16, 6.0), (32, 9.0)])
+@pytest.mark.parametrize("kind", ["smooth", "neareq", "random", "bkw"])
+def test_collide_2d(torch, fks, N, L, kind):
+    ncells = 13 if N < 32 else 7          # ragged against the cells-per-CTA grouping
+    f = workloads.family(kind, 2, N, L, ncells, seed=1)
+    ctx = fks.Context(2, 0, [ncells], N, L, 8)
+    Q = torch.empty(ncells, N, N, dtype=torch.float64, device="cuda")
+    ctx.collide(dev(torch, f), Q)
+    ctx.check()
+    tab = tables.build_tables(2, N, L, A=8)
+    assert rel_err_Q(host(Q), f, tab, direct=True) <= TOL
+
+
+@pytest.mark.parametrize("N,L", [(8, 7.0), (16, 7.0)])
+@pytest.mark.parametrize("kind", ["smooth", "neareq", "random"])
+def test_collide_3d_small(torch, fks, N, L, kind):
+    ncells = 11
+    f = workloads.family(kind, 3, N, L, ncells, seed=2)
+    ctx = fks.Context(3, 0, [ncells], N, L, 24)
+    Q = torch.empty(ncells, N, N, N, dtype=torch.float64, device="cuda")
+    ctx.collide(dev(torch, f), Q)
+    ctx.check()
+    tab = tables.build_tables(3, N, L)
+    assert rel_err_Q(host(Q), f, tab, direct=(N == 8)) <= TOL
+
+
+def test_collide_3d_product_directions(torch, fks):
+    """The (theta, phi) product grid of P:527-540 (A1 = A2 = 8, reading #6)."""
+    from oracle import kernels as okern
+    N, L, ncells = 8, 7.0, 5
+    f = workloads.family("random", 3, N, L, ncells, seed=3)
+    ctx = fks.Context(3, 0, [ncells], N, L, 64)
+    Q = torch.empty(ncells, N, N, N, dtype=torch.float64, device="cuda")
+    ctx.collide(dev(torch, f), Q)
+    tab = tables.build_tables(3, N, L, directions=okern.directions_3d_product(8, 8))
+    assert rel_err_Q(host(Q), f, tab, direct=True) <= TOL
+
+
+@pytest.mark.parametrize("kind", ["smooth", "random"])
+def test_collide_3d_32(torch, fks, kind):
+    """N = 32^3, 24-design (C2 shape), more cells than resident clusters (ragged tail)."""
+    N, L = 32, 7.0
+    ncells = 37
+    f = workloads.family(kind, 3, N, L, ncells, seed=4)
+    ctx = fks.Context(3, 0, [ncells], N, L, 24)
+    Q = torch.empty(ncells, N, N, N, dtype=torch.float64, device="cuda")
+    ctx.collide(dev(torch, f), Q)
+    ctx.check()
+    tab = tables.build_tables(3, N, L)
+    Qg = host(Q)
+    assert rel_err_Q(Qg[:12], f[:12], tab, direct=False) <= TOL
+    # one cell against modes of the literal double sum, computed one by one
+    modes = np.random.default_rng(0).choice(N ** 3, size=4, replace=False)
+    qh, _, ql = collision.qhat_direct(f[0], tab, modes=modes)
+    _, _, lf = collision.collide_fft(f[0], tab, return_parts=True)
+    got = (collision.dft(Qg[0]) / tab.scale).reshape(-1)[modes]
+    assert np.max(np.abs(got - qh)) <= TOL * np.max(np.abs(collision.dft(lf) / tab.scale))
+
+
+# ---------------------------------------------------------------- a3-a9: step
+def test_step_0d_3d_C2_cells(torch, fks):
+    c = workloads.config("C2")
+    N, L = c["N"], c["L"]
+    f = workloads.initial_state(c, ncells=19)
+    ctx = fks.Context(3, 0, [19], N, L, 24)
+    fin, fout = dev(torch, f), torch.empty(19, N, N, N, dtype=torch.float64, device="cuda")
+    ctx.step(fin, fout, c["dt"])
+    ctx.check()
+    tab = tables.build_tables(3, N, L)
+    ref = ostep.homogeneous_step(f, tab, c["dt"])
+    got = host(fout)
+    for i in range(19):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+    assert ctx.get_state()[0] == 1
+
+
+def test_step_0d_2d_C1_ten_steps(torch, fks):
+    """C1 literal run shape: BKW cells, 10 steps, growth of the difference reported (<= 1e-11)."""
+    c = workloads.config("C1")
+    N, L = c["N"], c["L"]
+    f = workloads.initial_state(c, ncells=7)
+    ctx = fks.Context(2, 0, [7], N, L, 8)
+    a, b = dev(torch, f), torch.empty(7, N, N, dtype=torch.float64, device="cuda")
+    tab = tables.build_tables(2, N, L, A=8)
+    ref = f.copy()
+    for s in range(10):
+        ctx.step(a, b, c["dt"])
+        a, b = b, a
+        ref = ostep.homogeneous_step(ref, tab, c["dt"])
+    got = host(a)
+    for i in range(7):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
+def _spatial_case(dxd, dv, M, N, L, bc, solid=None, seed=0):
+    rng = np.random.default_rng(100 + seed)
+    vmax = L - L / N
+    h = 0.1
+    dt = 0.93 * h / vmax
+    shape = tuple(M[::-1]) + (N,) * dv
+    base = workloads.family("smooth", dv, N, L, 1, seed=seed)[0]
+    F = base[None] * rng.uniform(0.5, 1.5, int(np.prod(M)))[(...,) + (None,) * dv]
+    F = F.reshape(shape)
+    ghosts = {f: workloads.family("smooth", dv, N, L, 1, seed=seed + 10 + f)[0] for f in range(2 * dxd)
+              if bc[f] == transport.GHOST}
+    return F, h, dt, ghosts
+
+
+@pytest.mark.parametrize("dxd,dv,M,N,bc", [
+    (1, 3, [12], 8, [transport.GHOST, transport.GHOST]),
+    (1, 2, [9], 16, [transport.PERIODIC, transport.PERIODIC]),
+    (2, 2, [5, 4], 8, [transport.GHOST, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC]),
+    (2, 3, [4, 3], 8, [transport.GHOST, transport.OUTFLOW, transport.OUTFLOW, transport.OUTFLOW]),
+    (3, 3, [3, 3, 3], 8, [transport.GHOST, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC,
+                          transport.OUTFLOW, transport.OUTFLOW]),
+])
+def test_step_with_transport(torch, fks, dxd, dv, M, N, bc):
+    """Three fused steps (a1..a9) with every face kind, against the oracle's split step."""
+    L = 6.0
+    F, h, dt, ghosts = _spatial_case(dxd, dv, M, N, L, bc, seed=dxd + dv)
+    solid = np.zeros(tuple(M[::-1]), dtype=bool)
+    if int(np.prod(M)) > 8:
+        solid.reshape(-1)[int(np.prod(M)) // 2] = True
+    ctx = fks.Context(dv, dxd, M, N, L, 8 if dv == 2 else 24, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_solid(solid)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    tab = tables.build_tables(dv, N, L, A=8) if dv == 2 else tables.build_tables(dv, N, L)
+    cfg = dict(dx_dim=dxd, dv=dv, N=N, L=L, dt=dt, dx=h, tau=1.0, bc=bc, ghosts=ghosts, solid=solid)
+    ref = F.copy()
+    for s in range(3):
+        ctx.step(a, b, dt)
+        a, b = b, a
+        ref = ostep.step(ref, s, cfg, tab)
+    got = host(a)
+    flat_g = got.reshape((-1,) + (N,) * dv)
+    flat_r = ref.reshape((-1,) + (N,) * dv)
+    for i in range(flat_r.shape[0]):
+        assert np.max(np.abs(flat_g[i] - flat_r[i])) <= TOL * np.max(np.abs(flat_r[i]))
+
+
+@pytest.mark.parametrize("dxd,dv,M,N,bc", [
+    (1, 3, [7], 8, [transport.GHOST, transport.OUTFLOW]),
+    (2, 2, [6, 5], 16, [transport.PERIODIC, transport.PERIODIC, transport.GHOST, transport.OUTFLOW]),
+    (3, 3, [4, 3, 2], 8, [transport.PERIODIC] * 2 + [transport.OUTFLOW, transport.GHOST] + [transport.PERIODIC] * 2),
+])
+def test_transport_bitwise(torch, fks, dxd, dv, M, N, bc):
+    """a1 + a3 alone: a permutation with boundary values, bitwise equal to the oracle over 7 steps."""
+    L = 5.0
+    F, h, dt, ghosts = _spatial_case(dxd, dv, M, N, L, bc, seed=7)
+    ctx = fks.Context(dv, dxd, M, N, L, 8 if dv == 2 else 24, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(7):
+        ctx.transport(a, b, dt)
+        a, b = b, a
+        ref = transport.gather(ref, s, dxd, dv, N, L, dt, h, bc, ghosts)
+    np.testing.assert_array_equal(host(a), ref)
+
+
+# ---------------------------------------------------------------- a10, flags, determinism, e2e
+def test_moments(torch, fks):
+    for dv, N, L in [(2, 32, 9.0), (3, 16, 7.0)]:
+        f = workloads.family("smooth", dv, N, L, 6, seed=5)
+        ctx = fks.Context(dv, 0, [6], N, L, 8 if dv == 2 else 24)
+        rho = torch.empty(6, dtype=torch.float64, device="cuda")
+        u = torch.empty(6, dv, dtype=torch.float64, device="cuda")
+        T = torch.empty(6, dtype=torch.float64, device="cuda")
+        ctx.moments(dev(torch, f), rho, u, T)
+        ro, uo, To = moments.moments_batch(f, dv, N, L)
+        np.testing.assert_allclose(host(rho), ro, rtol=1e-13)
+        np.testing.assert_allclose(host(u), uo, rtol=1e-12, atol=1e-13 * np.abs(uo).max())
+        np.testing.assert_allclose(host(T), To, rtol=1e-12)
+
+
+def test_nonfinite_flag(torch, fks):
+    N, L = 8, 7.0
+    f = workloads.family("smooth", 3, N, L, 3, seed=6)
+    f[1, 2, 3, 4] = np.nan
+    ctx = fks.Context(3, 0, [3], N, L, 24)
+    out = torch.empty(3, N, N, N, dtype=torch.float64, device="cuda")
+    ctx.step(dev(torch, f), out, 0.01)
+    with pytest.raises(fks.FksError) as ei:
+        ctx.check()
+    assert ei.value.status == -6
+    ctx.check()  # flag cleared
+
+
+def test_deterministic_and_host_path(torch, fks):
+    """Two runs are bitwise identical; fks_step_host (host buffers) equals the device path."""
+    c = workloads.config("C2")
+    N, L = c["N"], c["L"]
+    f = workloads.initial_state(c, ncells=21)
+    outs = []
+    for _ in range(2):
+        ctx = fks.Context(3, 0, [21], N, L, 24)
+        o = torch.empty(21, N, N, N, dtype=torch.float64, device="cuda")
+        ctx.step(dev(torch, f), o, c["dt"])
+        outs.append(host(o))
+    np.testing.assert_array_equal(outs[0], outs[1])
+    ctx = fks.Context(3, 0, [21], N, L, 24)
+    hin = torch.from_numpy(f.copy()).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    ctx.step_host(hin, hout, c["dt"])
+    np.testing.assert_array_equal(hout.numpy(), outs[0])
+
+
+def test_full_size_C2_launch_sampled(torch, fks):
+    """BASELINE configs[1] at full size (4096 cells) in bench.py's launch configuration; sampled
+    cells against the oracle one by one, plus exact mass conservation on every cell."""
+    c = workloads.config("C2")
+    N, L, nc = c["N"], c["L"], c["cells"][0]
+    f = workloads.initial_state(c)
+    ctx = fks.Context(3, 0, [nc], N, L, 24)
+    fin = dev(torch, f)
+    out = torch.empty_like(fin)
+    ctx.step(fin, out, c["dt"])
+    ctx.check()
+    tab = tables.build_tables(3, N, L)
+    got = host(out)
+    for i in [0, 1, 1777, nc - 1]:
+        ref = ostep.homogeneous_step(f[i:i + 1], tab, c["dt"])[0]
+        assert np.max(np.abs(got[i] - ref)) <= TOL * np.max(np.abs(ref))
+    mass_in = f.reshape(nc, -1).sum(axis=1)
+    mass_out = got.reshape(nc, -1).sum(axis=1)
+    assert np.max(np.abs(mass_out - mass_in) / mass_in) < 1e-12
