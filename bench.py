@@ -1,0 +1,287 @@
+"""Benchmark of the fused FKS + fast-spectral step on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+One "step" = one fks_step over the whole batch (all §8(a) rows the config has: transport with
+boundaries for C3-C5, collision a4-a7, projection a8, Euler a9).  Default workload: BASELINE.json
+configs[1] = C2 (0Dx3D hard-sphere two-Gaussian relaxation ensemble, Nv = 32^3, A = 24 spherical
+7-design directions), 4096 cells per GPU (1 GiB state, larger than L2), weak scaling across
+ranks with no collective on the data path.  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "collision evals/s (Nv=32³, M dirs) and phase-space updates/s at 1/2/4/8 B200"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# FP64 DFMA peak derived from unit counts and clocks (B200_PROFILING.md: 148 SMs, 1965 MHz max;
+# 64 DFMA/clk/SM), measured 37.1 TFLOP/s in profiles/r01_microbench.txt.
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def flops_per_cell(dv, N, A):
+    """SURVEY §8(a) / App. A.9 algorithmic flops per cell-step: (A+1) 5 n log2 n + (9A + 25) n."""
+    n = N ** dv
+    return (A + 1) * 5 * n * math.log2(n) + (9 * A + 25) * n
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--cells", type=int, default=0, help="override cells per GPU (0D configs)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    def __init__(self):
+        self.rows, self.proc = [], None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", os.environ.get("LOCAL_RANK", "0")],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle (CPU) timing
+def _oracle_worker(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    name, start, count, evaluator = args
+    import workloads
+    from oracle import step as ostep, tables
+    c = workloads.config(name)
+    f = workloads.initial_state(c, ncells=count, start=start)
+    tab = tables.build_tables(c["dv"], c["N"], c["L"], A=c["A"]) if c["dv"] == 2 else tables.build_tables(3, c["N"], c["L"])
+    t0 = time.perf_counter()
+    ostep.homogeneous_step(f, tab, c["dt"], c["tau"], evaluator=evaluator)
+    return time.perf_counter() - t0
+
+
+def oracle_rate(name, seconds=15.0, cores=None):
+    """cells/s of the oracle's fast evaluator (collide_fft + projection + Euler, numpy) over a
+    bounded sample, one single-threaded worker per host core."""
+    import multiprocessing as mp
+    import workloads
+    c = workloads.config(name)
+    cores = cores or os.cpu_count() or 1
+    # calibrate: one cell on one core
+    t1 = _oracle_worker((name, 0, 1, "fft"))
+    per_worker = max(1, int(seconds / max(t1, 1e-6) / 2))
+    tot = per_worker * cores
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        times = pool.map(_oracle_worker, [(name, (i * per_worker) % max(1, c["cells"][0] - per_worker), per_worker,
+                                           "fft") for i in range(cores)])
+    wall = max(times)  # workers run concurrently; each times only its own step loop
+    return tot / wall, cores, tot, wall
+
+
+# ------------------------------------------------------------------ main
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import workloads
+    c = workloads.config(a.config)
+    dv, N, A = c["dv"], c["N"], c["A"]
+    n = N ** dv
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        steps, warm = a.steps, a.warmup
+        budget = min(20.0, max(3.0, 120.0 / max(1, steps + warm)))
+        for _ in range(warm):
+            oracle_rate(a.config, seconds=min(budget, 5.0))
+        rates, cores_used, sample = [], 0, 0
+        for _ in range(steps):
+            r, cores_used, tot, wall = oracle_rate(a.config, seconds=budget)
+            rates.append(r)
+            sample = tot
+        val = sum(rates) / len(rates)
+        ms = 1e3 * c["cells"][0] / val
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "cells/s", "n_gpus": a.gpus,
+                "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{a.config} oracle step (collide_fft + projection + Euler, numpy fp64)",
+                           "cells_per_gpu": c["cells"][0], "Nv": N, "dv": dv, "M_dirs": A},
+                "phase_space_updates_per_s": val * n,
+                "cpu_baseline": {"value": val, "unit": "cells/s", "cores": cores_used, "kind": "oracle",
+                                 "sample": f"{sample} cells of {a.config} per step on {cores_used} single-threaded "
+                                           f"workers (ms_per_step extrapolated to {c['cells'][0]} cells)"},
+                "e2e": {"value": val, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import numpy as np
+    import torch
+    from paper_1608_08009_b200 import fks
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if c["dx_dim"] != 0:
+        raise SystemExit("bench.py times the 0D ensembles C1/C2 in round 1 (spatial configs: tests)")
+    ncells = a.cells or c["cells"][0]
+    # synthetic input: generate 256 distinct cells and tile them (generation of 4096 cells in
+    # numpy takes longer than the timed run); every cell still runs the full path
+    base = workloads.initial_state(c, ncells=min(ncells, 256), start=(rank * 256) % c["cells"][0])
+    reps = (ncells + base.shape[0] - 1) // base.shape[0]
+    F = np.concatenate([base] * reps)[:ncells]
+    ctx = fks.Context(dv, 0, [ncells], N, c["L"], A)
+    ctx.set_params(tau=c["tau"])
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream)
+    fa = torch.from_numpy(F).cuda()
+    fb = torch.empty_like(fa)
+    dt = c["dt"]
+
+    def one_step(x, y):
+        ctx.step(x, y, dt)
+
+    for _ in range(a.warmup):
+        one_step(fa, fb)
+        fa, fb = fb, fa
+    ctx.check()
+    clocks = Clocks()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = ctx.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(a.steps):
+        evs[i][0].record(stream)
+        one_step(fa, fb)
+        evs[i][1].record(stream)
+        fa, fb = fb, fa
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ctx.check()
+    launches = ctx.launch_count() - launches0
+    ms_total = t_start.elapsed_time(t_end)
+    kern_ms = [s.elapsed_time(e) for s, e in evs]
+    if dist:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / a.steps
+    value = ncells * world * a.steps / (ms_total * 1e-3)
+    fl = flops_per_cell(dv, N, A)
+    kern_avg_ms = sum(kern_ms) / len(kern_ms)
+    achieved = fl * ncells / (kern_avg_ms * 1e-3) / 1e12
+
+    # ---- e2e through the C ABI with host buffers (H2D + step + D2H per step) --------------
+    e2e = None
+    if not a.no_e2e:
+        hin = torch.from_numpy(F).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        ctx_h = fks.Context(dv, 0, [ncells], N, c["L"], A)
+        ctx_h.set_params(tau=c["tau"])
+        ctx_h.set_stream(stream)
+        ctx_h.step_host(hin, hout, dt)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ksteps = max(1, min(a.steps, 5))
+        for _ in range(ksteps):
+            ctx_h.step_host(hin, hout, dt)
+            hin, hout = hout, hin
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        bytes_ = ncells * n * 8
+        e2e = {"value": ncells * world * ksteps / el, "unit": "cells/s", "h2d_bytes_per_step": bytes_,
+               "d2h_bytes_per_step": bytes_, "steps": ksteps, "path": "fks_step_host (pinned host buffers)"}
+        ctx_h.close()
+
+    if rank == 0:
+        cpu = None
+        if not a.no_cpu_baseline and world == 1:
+            rate, cores, tot, wall = oracle_rate(a.config, seconds=15.0)
+            cpu = {"value": rate, "unit": "cells/s", "cores": cores, "kind": "oracle",
+                   "sample": f"{tot} cells of {a.config} (oracle collide_fft + projection + Euler, numpy fp64) "
+                             f"in {wall:.1f} s on {cores} single-threaded processes"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{a.config}: " + {
+                "C1": "0Dx2D BKW ensemble, Maxwell molecules, Nv=32^2, A=8",
+                "C2": "0Dx3D two-Gaussian relaxation ensemble (Test 1.3 shape), hard spheres, Nv=32^3, "
+                      "A=24 spherical 7-design"}.get(a.config, a.config),
+                "cells_per_gpu": ncells, "Nv": N, "dv": dv, "M_dirs": A, "dt": dt,
+                "l2": f"inputs larger than L2 ({2 * ncells * n * 8 / 2**30:.2f} GiB ping-pong state)",
+                "parallelism": f"dp{world} (independent cells, no collective)"},
+            "phase_space_updates_per_s": value * n,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "kernel": "k_step3d" if dv == 3 else "k_step2d",
+                         "flops_per_cell": fl, "kernel_ms_avg": kern_avg_ms,
+                         "note": "FP64 DFMA peak 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured 37.1); "
+                                 "flops in the 5 n log2 n FFT convention (SURVEY App. A.9)"},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

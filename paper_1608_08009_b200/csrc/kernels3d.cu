@@ -1,25 +1,31 @@
 // 3D fused collision / step kernel (a3-a9) for hard spheres on an N^3 velocity grid.
 //
-// One thread-block cluster of P = 8 CTAs owns one cell at a time (persistent over cells).
-// The cell's N^3 spectrum does not fit one SM (N = 32: 512 KiB per complex transform), so the
+// One thread-block cluster of P CTAs owns one cell at a time (persistent over cells).  The
+// cell's N^3 spectrum does not fit one SM (N = 32: 512 KiB per complex transform), so the
 // 3D inverse FFT of each direction is split by planes:
 //   CTA r owns the spectrum planes l_y in [r N/P, (r+1) N/P)  (f^ resident in SMEM) and
-//   the output planes  j_z in [r N/P, (r+1) N/P)             (gain accumulator G in SMEM).
+//   the output planes  j_z in [r N/P, (r+1) N/P)             (gain accumulator in registers).
 // Per direction p the CTA
-//   (1) forms X = (alpha~_p + i alpha'~_p) f^ on its pencils and does the z-IFFT in registers,
-//   (2) writes the pencils to a per-cluster L2 exchange buffer (the transpose),
-//   (3) cluster barrier, then reads its own j_z planes and does the x- and y-IFFTs,
-//   (4) accumulates G += Re z * Im z (two real transforms packed in one complex IFFT; exact
-//       because the symmetrised tables are real and even, reading #10).
-// The exchange goes through L2 (measured ~15 TB/s) rather than DSMEM (measured ~2 TB/s,
-// profiles/r01_microbench.txt).  The next direction's table slab is prefetched into SMEM with
-// a bulk async copy (cp.async.bulk, completion on an mbarrier) while the xy-pass runs.
-// The loss is the (A+1)-th "direction" with table (D~, 0): Q = G - f* Re z.
-// The epilogue projects Q to zero moments (a cluster-wide 5-sum reduction through
-// DSMEM) and writes F^{n+1} = f* + (dt/tau) Pi Q, or writes Q (collide mode).
+//   z: forms X = (alpha~_p + i alpha'~_p) f^ on its pencils and IFFTs along z in registers,
+//      then writes the pencils to a per-cluster L2 exchange buffer (the transpose);
+//   xy: after a cluster barrier, bulk-copies its own j_z planes back (cp.async.bulk, async
+//      proxy), IFFTs along x and y and accumulates G += Re z * Im z -- two real transforms
+//      packed in one complex IFFT, exact because the symmetrised tables are real and even
+//      (reading #10).
+// Software pipeline (per cell, d = 0..A, the loss is d = A with table (D~, 0)):
+//   z(0); arrive(0);
+//   for d: wait(d); bulk W(d) -> SMEM; z(d+1) [overlaps the copy]; xy(d); arrive(d+1)
+// so the exchange latency hides behind z(d+1) and the release fence of arrive(d+1) finds the
+// z(d+1) stores long completed.  The exchange goes through L2 (measured ~15 TB/s) rather than
+// DSMEM (measured ~2 TB/s, profiles/r01_microbench.txt).  The next direction's table slab is
+// prefetched with cp.async.bulk while xy runs.  Epilogue: Q = G - f* Re z(loss),
+// projection to zero moments (5-sum cluster reduction through DSMEM) and
+// F^{n+1} = f* + (dt/tau) Pi Q, or Q in collide mode.
 // Tables are pre-folded on the host: alpha~ = s w_p alpha_p / n, alpha'~ = alpha'_p / n,
 // D~ = s D / n (s = Btilde kappa^-(d+gamma)); layout T[p][l_y][l_z][l_x] as double2.
 #include <cooperative_groups.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -33,23 +39,24 @@ template <int N, int P>
 struct Cfg3 {
   static constexpr int NP = N / P;        // planes per CTA
   static constexpr int THREADS = N * NP;  // one pencil / row / column per thread
-  static constexpr int PLANE = N * N;
-  static constexpr int SLAB = NP * PLANE;     // complex elements per CTA slab
-  static constexpr int RS = N + 1;            // padded row stride of the xy-pass buffer
-  static constexpr int PSLAB = NP * N * RS;   // padded slab
-  static constexpr size_t OFF_FHAT = 0;
+  static constexpr int RS = N + 1;        // padded row stride (bank-conflict-free rows and columns)
+  static constexpr int SLAB = NP * N * N;     // complex elements of f^ / table slab
+  static constexpr int PSLAB = NP * N * RS;   // complex elements of a padded plane slab
+  static constexpr int WPLANE = N * RS;       // padded plane in the exchange buffer
+  static constexpr size_t WBUF = (size_t)N * WPLANE;  // one exchange buffer (all N j_z planes)
+  static constexpr int NBUF = 2;
+  static constexpr size_t OFF_FHAT = 0;  // f^ slab; reused as G/Q after the last z-pass
   static constexpr size_t OFF_TBUF = OFF_FHAT + (size_t)SLAB * 16;
   static constexpr size_t OFF_PLN = OFF_TBUF + (size_t)SLAB * 16;
-  static constexpr size_t OFF_G = OFF_PLN + (size_t)PSLAB * 16;
-  static constexpr size_t OFF_MBAR = OFF_G + (size_t)SLAB * 8;
+  static constexpr size_t OFF_MBAR = OFF_PLN + (size_t)PSLAB * 16;
   static constexpr size_t OFF_PART = OFF_MBAR + 16;
   static constexpr size_t SMEM = OFF_PART + 8 * 8;
+  static_assert((size_t)NP * N * N * 8 <= (size_t)SLAB * 16, "G must fit in the f^ slab");
 };
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() { cl_arrive(); cl_wait(); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -85,17 +92,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-template <int N, int P>
-__device__ __forceinline__ void load_table_slab(double2* tbuf, const double2* tables, int p, int rank,
-                                                uint64_t* bar) {
-  using C = Cfg3<N, P>;
-  constexpr uint32_t bytes = C::SLAB * 16;
-  constexpr uint32_t chunk = bytes > 16384 ? 16384 : bytes;
-  const double2* src = tables + (size_t)p * N * N * N + (size_t)rank * C::SLAB;
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  constexpr uint32_t chunk = 32768;
   mbar_expect_tx(bar, bytes);
-#pragma unroll 1
   for (uint32_t off = 0; off < bytes; off += chunk)
-    bulk_g2s(reinterpret_cast<char*>(tbuf) + off, reinterpret_cast<const char*>(src) + off, chunk, bar);
+    bulk_g2s(reinterpret_cast<char*>(dst) + off, reinterpret_cast<const char*>(src) + off,
+             bytes - off < chunk ? bytes - off : chunk, bar);
+}
+
+// One pencil (l_x = tx, local l_y = tl) of direction d: X = T (x) f^, IFFT along z, store to W.
+template <int N, int P>
+__device__ __forceinline__ void zpass(const double2* fhat, const double2* tbuf, double2* Wb, int rank, int tx,
+                                      int tl) {
+  using C = Cfg3<N, P>;
+  double2 x[N];
+  const double2* fh = fhat + tl * N * N + tx;
+  const double2* tb = tbuf + tl * N * N + tx;
+#pragma unroll
+  for (int lz = 0; lz < N; ++lz) {
+    const double2 T = tb[lz * N], F = fh[lz * N];
+    x[lz] = make_double2(fma(T.x, F.x, -T.y * F.y), fma(T.x, F.y, T.y * F.x));
+  }
+  fft<N, +1>(x);
+  double2* w = Wb + (size_t)(rank * C::NP + tl) * C::RS + tx;
+#pragma unroll
+  for (int jz = 0; jz < N; ++jz) w[(size_t)jz * C::WPLANE] = x[jz];
 }
 
 template <int N, int P>
@@ -105,10 +126,11 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   constexpr int n = N * N * N;
   extern __shared__ __align__(128) unsigned char smem[];
   double2* fhat = reinterpret_cast<double2*>(smem + C::OFF_FHAT);  // [NP l_y][N l_z][N l_x]
+  double* G = reinterpret_cast<double*>(smem + C::OFF_FHAT);       // [NP j_z][N j_y][N j_x] (after z(A))
   double2* tbuf = reinterpret_cast<double2*>(smem + C::OFF_TBUF);  // [NP l_y][N l_z][N l_x]
   double2* pln = reinterpret_cast<double2*>(smem + C::OFF_PLN);    // [NP j_z][N y][RS x]
-  double* G = reinterpret_cast<double*>(smem + C::OFF_G);          // [NP j_z][N j_y][N j_x]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
+  uint64_t* wbar = tbar + 1;
   double* part = reinterpret_cast<double*>(smem + C::OFF_PART);
 
   cg::cluster_group cluster = cg::this_cluster();
@@ -116,28 +138,46 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   const int cid = blockIdx.x / P;
   const int ncl = gridDim.x / P;
   const int t = threadIdx.x;
-  const int tx = t % N;   // l_x / j_x / row index along the fast axis
-  const int tl = t / N;   // local plane index
-  double2* W = p.scratch + (size_t)cid * 2 * n;  // [2][N j_z][N l_y][N l_x]
+  const int tx = t % N;  // l_x / j_x / row index along the fast axis
+  const int tl = t / N;  // local plane index
+  double2* Wbase = p.scratch + (size_t)cid * C::NBUF * C::WBUF;  // [NBUF][N j_z][N l_y][RS l_x]
+  constexpr uint32_t kTabBytes = C::SLAB * 16;
+  constexpr uint32_t kPlaneBytes = C::PSLAB * 16;
 
   if (t == 0) {
-    mbar_init(mbar, 1);
+    mbar_init(tbar, 1);
+    mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  uint32_t tphase = 0;
+  uint32_t tphase = 0, wphase = 0;
   int buf = 0;
 
   for (int it = cid; it < p.ncells; it += ncl) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
-    if (t == 0) load_table_slab<N, P>(tbuf, p.tables, 0, rank, mbar);
+    if (t == 0)
+      bulk_load(tbuf, p.tables + (size_t)rank * C::SLAB, kTabBytes, tbar);
 
-    // ---- a3 + a4: gather f* (own j_z planes) and forward FFT in x and y --------------------
-    for (int e = t; e < C::SLAB; e += C::THREADS) {
-      const int x = e % N, y = (e / N) % N, zl = e / (N * N);
-      const int z = rank * NP + zl;
-      const double v = gather_fstar(p.f_in, p.tp, cell, x + N * (y + N * z), x, y, z, n);
-      pln[zl * N * RS + y * RS + x] = make_double2(v, 0.0);
+    // ---- a3 + a4: gather f* (own j_z planes) and forward FFT in x, y, then z -------------
+    {
+      constexpr int PER = NP * N * N / C::THREADS;  // = N: elements per thread
+      constexpr int B = PER < 16 ? PER : 16;        // loads in flight per batch
+#pragma unroll 1
+      for (int b0 = 0; b0 < PER; b0 += B) {
+        double v[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int e = t + (b0 + j) * C::THREADS;
+          const int x = e % N, y = (e / N) % N, z = rank * NP + e / (N * N);
+          v[j] = gather_fstar(p.f_in, p.tp, cell, x + N * (y + N * z), x, y, z, n);
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int e = t + (b0 + j) * C::THREADS;
+          const int x = e % N, y = (e / N) % N, zl = e / (N * N);
+          pln[zl * N * RS + y * RS + x] = make_double2(v[j], 0.0);
+        }
+      }
     }
     __syncthreads();
     {
@@ -156,57 +196,54 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
 #pragma unroll
       for (int y = 0; y < N; ++y) c[y] = col[y * RS];
       fft<N, -1>(c);
-      double2* Wb = W + (size_t)buf * n + (size_t)(rank * NP + tl) * N * N + tx;
+      double2* Wb = Wbase + (size_t)buf * C::WBUF + (size_t)(rank * NP + tl) * C::WPLANE + tx;
 #pragma unroll
-      for (int ly = 0; ly < N; ++ly) Wb[ly * N] = c[ly];
+      for (int ly = 0; ly < N; ++ly) Wb[ly * RS] = c[ly];
     }
     cluster_sync_all();
     {
-      // z-FFT of pencil (l_x = tx, l_y = rank*NP + tl)
       double2 c[N];
-      const double2* Wb = W + (size_t)buf * n + (size_t)(rank * NP + tl) * N + tx;
+      const double2* Wb = Wbase + (size_t)buf * C::WBUF + (size_t)(rank * NP + tl) * RS + tx;
 #pragma unroll
-      for (int z = 0; z < N; ++z) c[z] = __ldcg(Wb + (size_t)z * N * N);
+      for (int z = 0; z < N; ++z) c[z] = __ldcg(Wb + (size_t)z * C::WPLANE);
       fft<N, -1>(c);
       double2* fh = fhat + tl * N * N + tx;
 #pragma unroll
       for (int lz = 0; lz < N; ++lz) fh[lz * N] = c[lz];
     }
     buf ^= 1;
+    __syncthreads();  // f^ complete
 
-    // ---- a5/a6: A gain directions + the loss ---------------------------------------------
+    // ---- a5/a6: A gain directions + the loss, software-pipelined --------------------------
+    mbar_wait(tbar, tphase);
+    tphase ^= 1;
+    zpass<N, P>(fhat, tbuf, Wbase + (size_t)buf * C::WBUF, rank, tx, tl);
+    __syncthreads();
+    if (t == 0) bulk_load(tbuf, p.tables + (size_t)1 * n + (size_t)rank * C::SLAB, kTabBytes, tbar);
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    cl_arrive();
+
     double gacc[N];
 #pragma unroll
     for (int y = 0; y < N; ++y) gacc[y] = 0.0;
 #pragma unroll 1
     for (int d = 0; d <= p.A; ++d) {
-      mbar_wait(mbar, tphase);
-      tphase ^= 1;
-      {
-        double2 x[N];
-        const double2* fh = fhat + tl * N * N + tx;
-        const double2* tb = tbuf + tl * N * N + tx;
-#pragma unroll
-        for (int lz = 0; lz < N; ++lz) {
-          const double2 T = tb[lz * N], F = fh[lz * N];
-          x[lz] = make_double2(fma(T.x, F.x, -T.y * F.y), fma(T.x, F.y, T.y * F.x));
-        }
-        fft<N, +1>(x);
-        double2* Wb = W + (size_t)buf * n + (size_t)(rank * NP + tl) * N + tx;
-#pragma unroll
-        for (int jz = 0; jz < N; ++jz) Wb[(size_t)jz * N * N] = x[jz];
+      const int bd = buf;  // exchange buffer of direction d
+      cl_wait();           // W(d) complete cluster-wide; W(d-1) no longer read anywhere
+      if (t == 0) {
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        bulk_load(pln, Wbase + (size_t)bd * C::WBUF + (size_t)rank * C::PSLAB, kPlaneBytes, wbar);
       }
-      __syncthreads();  // tbuf consumed
-      if (t == 0 && d < p.A) load_table_slab<N, P>(tbuf, p.tables, d + 1, rank, mbar);
-      cluster_sync_all();
-      {
-        const double2* Wp = W + (size_t)buf * n + (size_t)rank * C::SLAB;
-        for (int e = t; e < C::SLAB; e += C::THREADS) {
-          const int x = e % N, yz = e / N;
-          pln[yz * RS + x] = __ldcg(Wp + e);
-        }
+      if (d < p.A) {
+        mbar_wait(tbar, tphase);
+        tphase ^= 1;
+        zpass<N, P>(fhat, tbuf, Wbase + (size_t)(bd ^ 1) * C::WBUF, rank, tx, tl);
+        __syncthreads();  // tbuf consumed
+        if (t == 0 && d + 2 <= p.A)
+          bulk_load(tbuf, p.tables + (size_t)(d + 2) * n + (size_t)rank * C::SLAB, kTabBytes, tbar);
       }
-      __syncthreads();
+      mbar_wait(wbar, wphase);
+      wphase ^= 1;
       {
         double2 r[N];
         double2* row = pln + tl * N * RS + tx * RS;
@@ -222,6 +259,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
         const double2* col = pln + tl * N * RS + tx;
 #pragma unroll
         for (int y = 0; y < N; ++y) c[y] = col[y * RS];
+        __syncthreads();  // pln free for the next bulk copy
         fft<N, +1>(c);
         if (d < p.A) {
 #pragma unroll
@@ -229,15 +267,23 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
         } else {
           const int z = rank * NP + tl;
           double* g = G + tl * N * N + tx;
+          double fs[N];
+#pragma unroll
+          for (int y = 0; y < N; ++y) fs[y] = gather_fstar(p.f_in, p.tp, cell, tx + N * (y + N * z), tx, y, z, n);
 #pragma unroll
           for (int y = 0; y < N; ++y) {
-            const double fs = gather_fstar(p.f_in, p.tp, cell, tx + N * (y + N * z), tx, y, z, n);
-            g[y * N] = gacc[y] - fs * c[y].x;
+            g[y * N] = gacc[y] - fs[y] * c[y].x;
+            gacc[y] = fs[y];  // gacc now holds the f* column for the Euler update
           }
         }
       }
       buf ^= 1;
+      if (d < p.A) {
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        cl_arrive();  // z(d+1) stores (issued before xy(d)) are complete by now
+      }
     }
+    __syncthreads();
 
     // ---- a8 + a9: projection and Euler (or write Q) ---------------------------------------
     const int z = rank * NP + tl;
@@ -259,13 +305,14 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
           m[3] += vz * q;
           m[4] += (vx * vx + vy * vy + vz * vz) * q;
         }
+        constexpr int W = C::THREADS < 32 ? C::THREADS : 32;
+        constexpr unsigned mask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
 #pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
+          for (int o = W / 2; o >= 1; o >>= 1) m[c] += __shfl_xor_sync(mask, m[c], o);
         }
         // warps -> CTA partial (fixed order), then the cluster sum through DSMEM in rank order
-        __syncthreads();
         constexpr int NW = (C::THREADS + 31) / 32;
         double* wpart = reinterpret_cast<double*>(pln);  // scratch: [NW][5]
         if ((t & 31) == 0) {
@@ -297,85 +344,99 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
       }
       const double vx = node_v(tx, p.L, p.dv), vz = node_v(z, p.L, p.dv);
       bool bad = false;
+#pragma unroll
       for (int y = 0; y < N; ++y) {
         const double vy = node_v(y, p.L, p.dv);
         const int k = tx + N * (y + N * z);
         const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * vz + lam[4] * (vx * vx + vy * vy + vz * vz);
-        const double fs = gather_fstar(p.f_in, p.tp, cell, k, tx, y, z, n);
-        const double o = fma(p.dt_tau, g[y * N] - corr, fs);
+        const double o = fma(p.dt_tau, g[y * N] - corr, gacc[y]);
         bad |= !isfinite(o);
         out[k] = o;
       }
       if (bad) atomicOr(p.nonfinite, 1);
-      if (p.project) cluster_sync_all();  // part[] is read remotely before it is rewritten
+      if (p.project) {  // part[] is read remotely before it is rewritten (or the CTA exits);
+        // the remote loads completed (their values were consumed), so no release is needed
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+        cl_wait();
+      }
     }
+    __syncthreads();  // G (= f^ slab) consumed before the next cell's f^
   }
 }
 
-template <int N>
-static cudaError_t launch3(const StepParams& p, int nclusters, cudaStream_t s) {
-  constexpr int P = 8;
+template <int N, int P>
+static cudaLaunchConfig_t make_cfg(int nclusters, cudaStream_t s, cudaLaunchAttribute* attr) {
   using C = Cfg3<N, P>;
-  auto kern = k_step3d<N, P>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nclusters * P);
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = P;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p);
+  return cfg;
 }
 
-template <int N>
-static int max_clusters3() {
-  constexpr int P = 8;
+template <int N, int P>
+static cudaError_t prep() {
   using C = Cfg3<N, P>;
   auto kern = k_step3d<N, P>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
-    return 0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(P * 64);
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (e != cudaSuccess) return e;
+  if (P > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
+
+template <int N, int P>
+static cudaError_t launch3(const StepParams& p, int nclusters, cudaStream_t s) {
+  cudaError_t e = prep<N, P>();
+  if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = P;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchConfig_t cfg = make_cfg<N, P>(nclusters, s, attr);
+  return cudaLaunchKernelEx(&cfg, k_step3d<N, P>, p);
+}
+
+template <int N, int P>
+static int max_clusters3() {
+  if (prep<N, P>() != cudaSuccess) return 0;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = make_cfg<N, P>(64, 0, attr);
   int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, k_step3d<N, P>, &cfg) != cudaSuccess) return 0;
   return ncl;
+}
+
+// CTAs per cell for N = 32 (8 or 16); 8 for the small grids.  FKS_P32 env var overrides (tuning).
+static int p32() {
+  static int v = [] {
+    const char* e = getenv("FKS_P32");
+    return (e && atoi(e) == 16) ? 16 : 8;
+  }();
+  return v;
 }
 
 cudaError_t launch_step3d(int N, const StepParams& p, int nclusters, cudaStream_t s) {
   switch (N) {
-    case 8: return launch3<8>(p, nclusters, s);
-    case 16: return launch3<16>(p, nclusters, s);
-    case 32: return launch3<32>(p, nclusters, s);
+    case 8: return launch3<8, 8>(p, nclusters, s);
+    case 16: return launch3<16, 8>(p, nclusters, s);
+    case 32: return p32() == 16 ? launch3<32, 16>(p, nclusters, s) : launch3<32, 8>(p, nclusters, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 int max_active_clusters3d(int N) {
   switch (N) {
-    case 8: return max_clusters3<8>();
-    case 16: return max_clusters3<16>();
-    case 32: return max_clusters3<32>();
+    case 8: return max_clusters3<8, 8>();
+    case 16: return max_clusters3<16, 8>();
+    case 32: return p32() == 16 ? max_clusters3<32, 16>() : max_clusters3<32, 8>();
     default: return 0;
   }
 }
 
-size_t scratch_elems3d(int N) { return (size_t)2 * N * N * N; }
+size_t scratch_elems3d(int N) { return (size_t)Cfg3<32, 8>::NBUF * N * N * (N + 1); }
 
 }  // namespace fks
