@@ -22,6 +22,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "collision evals/s (Nv=32³, M dirs) and phase-space updates/s at 1/2/4/8 B200"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_SUMMARY = {3: os.path.join(ROOT, "profiles", "r01_ncu_k_step3d.json")}
+
+
+def dram_traffic(dv, ncells):
+    """dram__bytes_read + dram__bytes_write per launch from the committed `ncu --set full` capture
+    of the dominant kernel (per-cell figure x cells of this launch), or None."""
+    path = NCU_SUMMARY.get(dv)
+    if not path or not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return json.load(fh)["dram_bytes_per_cell"] * ncells
 # FP64 DFMA peak derived from unit counts and clocks (B200_PROFILING.md: 148 SMs, 1965 MHz max;
 # 64 DFMA/clk/SM), measured 37.1 TFLOP/s in profiles/r01_microbench.txt.
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
@@ -268,7 +279,9 @@ def main():
                 "parallelism": f"dp{world} (independent cells, no collective)"},
             "phase_space_updates_per_s": value * n,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": dram_traffic(dv, ncells),
+                         "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01_ncu_k_step3d.json)",
+                         "algorithmic_bytes": 2 * n * 8 * ncells,
                          "kernel": "k_step3d" if dv == 3 else "k_step2d",
                          "flops_per_cell": fl, "kernel_ms_avg": kern_avg_ms,
                          "note": "FP64 DFMA peak 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured 37.1); "

@@ -12,13 +12,18 @@
 //      proxy), IFFTs along x and y and accumulates G += Re z * Im z -- two real transforms
 //      packed in one complex IFFT, exact because the symmetrised tables are real and even
 //      (reading #10).
-// Software pipeline (per cell, d = 0..A, the loss is d = A with table (D~, 0)):
-//   z(0); arrive(0);
-//   for d: wait(d); bulk W(d) -> SMEM; z(d+1) [overlaps the copy]; xy(d); arrive(d+1)
-// so the exchange latency hides behind z(d+1) and the release fence of arrive(d+1) finds the
-// z(d+1) stores long completed.  The exchange goes through L2 (measured ~15 TB/s) rather than
-// DSMEM (measured ~2 TB/s, profiles/r01_microbench.txt).  The next direction's table slab is
-// prefetched with cp.async.bulk while xy runs.  Epilogue: Q = G - f* Re z(loss),
+// Warp specialisation and pipeline (per cell, D = A + 1 exchanges, the loss is the last one,
+// with table (D~, 0)).  The CTA has a z group and an xy group of N*NP threads each; phase k of
+// the cluster barrier completes when every z group has stored z(k) and every xy group has
+// finished xy(k-2):
+//   z group : arrive k; compute z(k+1) in registers (overlaps the barrier); wait k; store z(k+1)
+//   xy group: xy(k-2) from plane buffer (k-2)%2; arrive k; wait k; bulk-copy W(k) -> buffer k%2
+// so every exchange copy lands while the previous direction is being transformed, and the
+// z group's FFT overlaps the barrier.  Three exchange buffers per cluster.  The per-cell f^
+// slab lives in tensor memory (TMEM, 128 columns x 128 lanes: one pencil per z-group lane,
+// tcgen05.st / tcgen05.ld), which frees shared memory for the double-buffered plane slabs and
+// the bulk-prefetched table slab.  The exchange goes through L2 (measured ~15 TB/s) rather than
+// DSMEM (measured ~2 TB/s, profiles/r01_microbench.txt).  Epilogue: Q = G - f* Re z(loss),
 // projection to zero moments (5-sum cluster reduction through DSMEM) and
 // F^{n+1} = f* + (dt/tau) Pi Q, or Q in collide mode.
 // Tables are pre-folded on the host: alpha~ = s w_p alpha_p / n, alpha'~ = alpha'_p / n,
@@ -35,24 +40,50 @@ namespace cg = cooperative_groups;
 
 namespace fks {
 
+// Development instrumentation: per-phase clock64 stamps of cluster 0 / CTA 0 (FKS_TIMING builds only).
+#ifdef FKS_TIMING
+__device__ long long g_tstamp[4096];
+#define TSTAMP(slot) do { if (cid == 0 && rank == 0 && (tg == 0) && it == 0) g_tstamp[(slot)] = clock64(); } while (0)
+#else
+#define TSTAMP(slot) do { } while (0)
+#endif
+
 template <int N, int P>
 struct Cfg3 {
   static constexpr int NP = N / P;        // planes per CTA
-  static constexpr int THREADS = N * NP;  // one pencil / row / column per thread
+  static constexpr int GT = N * NP;       // threads per warp group (one pencil / row / column each)
+  static constexpr int THREADS = 2 * GT;  // z group + xy group (warp-specialised)
   static constexpr int RS = N + 1;        // padded row stride (bank-conflict-free rows and columns)
-  static constexpr int SLAB = NP * N * N;     // complex elements of f^ / table slab
+  static constexpr int SLAB = NP * N * N;     // complex elements of the f^ / table slab
   static constexpr int PSLAB = NP * N * RS;   // complex elements of a padded plane slab
   static constexpr int WPLANE = N * RS;       // padded plane in the exchange buffer
   static constexpr size_t WBUF = (size_t)N * WPLANE;  // one exchange buffer (all N j_z planes)
-  static constexpr int NBUF = 2;
-  static constexpr size_t OFF_FHAT = 0;  // f^ slab; reused as G/Q after the last z-pass
-  static constexpr size_t OFF_TBUF = OFF_FHAT + (size_t)SLAB * 16;
-  static constexpr size_t OFF_PLN = OFF_TBUF + (size_t)SLAB * 16;
-  static constexpr size_t OFF_MBAR = OFF_PLN + (size_t)PSLAB * 16;
-  static constexpr size_t OFF_PART = OFF_MBAR + 16;
+  static constexpr int NBUF = 4;  // z stores z(k+1) while phase k is still completing
+  static constexpr int TMEM_COLS = 4 * N;     // one f^ pencil (N complex fp64) per lane
+  static constexpr size_t OFF_TBUF = 0;
+  static constexpr size_t OFF_PLN = OFF_TBUF + (size_t)SLAB * 16;  // two plane slabs
+  static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;  // tbar, wbar[2]
+  static constexpr size_t OFF_TMEM = OFF_MBAR + 24;
+  static constexpr size_t OFF_PART = OFF_TMEM + 8;
   static constexpr size_t SMEM = OFF_PART + 8 * 8;
-  static_assert((size_t)NP * N * N * 8 <= (size_t)SLAB * 16, "G must fit in the f^ slab");
+  static_assert(GT % 32 == 0, "warp groups must be whole warps");
+  static_assert(GT <= 128, "one TMEM lane per z-group thread");
+  static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM allocation: power of two >= 32");
 };
+
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// TMEM (tcgen05) helpers: 32 columns (32-bit each) of this thread's lane.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
@@ -100,256 +131,315 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
              bytes - off < chunk ? bytes - off : chunk, bar);
 }
 
-// One pencil (l_x = tx, local l_y = tl) of direction d: X = T (x) f^, IFFT along z, store to W.
+// z group: X = T (x) f^ for pencil (l_x = tx, local l_y = tl) of one direction (f^ from this
+// thread's TMEM lane, T from the SMEM table slab), then the IFFT along z, in registers.
 template <int N, int P>
-__device__ __forceinline__ void zpass(const double2* fhat, const double2* tbuf, double2* Wb, int rank, int tx,
-                                      int tl) {
-  using C = Cfg3<N, P>;
-  double2 x[N];
-  const double2* fh = fhat + tl * N * N + tx;
+__device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbuf, int tx, int tl, double2 (&x)[N]) {
   const double2* tb = tbuf + tl * N * N + tx;
 #pragma unroll
-  for (int lz = 0; lz < N; ++lz) {
-    const double2 T = tb[lz * N], F = fh[lz * N];
-    x[lz] = make_double2(fma(T.x, F.x, -T.y * F.y), fma(T.x, F.y, T.y * F.x));
+  for (int ch = 0; ch < N / 8; ++ch) {  // 8 complex fp64 = 32 TMEM columns per chunk
+    uint32_t v[32];
+    tmem_ld32(taddr + ch * 32, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int lz = ch * 8 + i;
+      const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
+      const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
+      const double2 T = tb[lz * N];
+      x[lz] = make_double2(fma(T.x, Fx, -T.y * Fy), fma(T.x, Fy, T.y * Fx));
+    }
   }
   fft<N, +1>(x);
+}
+
+// z-pass output -> this CTA's rows of the exchange buffer (L2): 32 coalesced 512-byte warp stores.
+// L2 write bandwidth (~7.8 TB/s chip-wide, tools/microbench/mb_store.cu) bounds the exchange;
+// staging through SMEM + bulk (TMA) stores was measured slower: the TMA engine reads the staging
+// buffer only as fast as it drains to L2, so the staging slot is not freed any earlier.
+template <int N, int P>
+__device__ __forceinline__ void zpass_store(const double2 (&x)[N], double2* Wb, int rank, int tx, int tl) {
+  using C = Cfg3<N, P>;
   double2* w = Wb + (size_t)(rank * C::NP + tl) * C::RS + tx;
 #pragma unroll
   for (int jz = 0; jz < N; ++jz) w[(size_t)jz * C::WPLANE] = x[jz];
 }
 
+// Shared-memory carve-up and per-thread coordinates of the 3D kernel.
 template <int N, int P>
-__global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepParams p) {
+struct Ctx3 {
   using C = Cfg3<N, P>;
-  constexpr int NP = C::NP, RS = C::RS;
-  constexpr int n = N * N * N;
-  extern __shared__ __align__(128) unsigned char smem[];
-  double2* fhat = reinterpret_cast<double2*>(smem + C::OFF_FHAT);  // [NP l_y][N l_z][N l_x]
-  double* G = reinterpret_cast<double*>(smem + C::OFF_FHAT);       // [NP j_z][N j_y][N j_x] (after z(A))
-  double2* tbuf = reinterpret_cast<double2*>(smem + C::OFF_TBUF);  // [NP l_y][N l_z][N l_x]
-  double2* pln = reinterpret_cast<double2*>(smem + C::OFF_PLN);    // [NP j_z][N y][RS x]
-  uint64_t* tbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
-  uint64_t* wbar = tbar + 1;
-  double* part = reinterpret_cast<double*>(smem + C::OFF_PART);
+  double2* tbuf;   // [NP l_y][N l_z][N l_x] table slab of the current direction
+  double2* pln0;   // 2 x [NP j_z][N y][RS x] plane slabs
+  uint64_t* tbar;  // table slab landed
+  uint64_t* wbar;  // [2] plane slab landed
+  double* part;    // [5] this CTA's moment partial sums (read through DSMEM)
+  double2* W;      // [NBUF][N j_z][N l_y][RS l_x] exchange buffers of this cluster (L2)
+  int rank, cid, ncl, tg, tx, tl;
+};
 
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int cid = blockIdx.x / P;
-  const int ncl = gridDim.x / P;
-  const int t = threadIdx.x;
-  const int tx = t % N;  // l_x / j_x / row index along the fast axis
-  const int tl = t / N;  // local plane index
-  double2* Wbase = p.scratch + (size_t)cid * C::NBUF * C::WBUF;  // [NBUF][N j_z][N l_y][RS l_x]
-  constexpr uint32_t kTabBytes = C::SLAB * 16;
-  constexpr uint32_t kPlaneBytes = C::PSLAB * 16;
-
-  if (t == 0) {
-    mbar_init(tbar, 1);
-    mbar_init(wbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+// Epilogue moment reduction (a8): xy group supplies m[5] (zeros from the z group); returns
+// lambda = Ginv * sum over the cluster (fixed order: warps, then ranks).
+template <int N, int P>
+__device__ __forceinline__ void project_lambda(const StepParams& p, const Ctx3<N, P>& c, bool xy, double (&m)[5],
+                                               double (&lam)[5]) {
+  using C = Cfg3<N, P>;
+  constexpr int NW = C::GT / 32;
+  double* wpart = reinterpret_cast<double*>(c.pln0);  // plane buffers idle in the epilogue
+  if (xy) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
+    }
+    if ((c.tg & 31) == 0) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) wpart[(c.tg >> 5) * 5 + k] = m[k];
+    }
   }
   __syncthreads();
-  uint32_t tphase = 0, wphase = 0;
-  int buf = 0;
+  if (threadIdx.x < 5) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += wpart[w * 5 + threadIdx.x];
+    c.part[threadIdx.x] = s;
+  }
+  cluster_sync_all();
+  cg::cluster_group cluster = cg::this_cluster();
+  double mu[5] = {0, 0, 0, 0, 0};
+  for (int r = 0; r < P; ++r) {
+    const double* rp = cluster.map_shared_rank(c.part, r);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) mu[k] += rp[k];
+  }
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) s = fma(p.Ginv[a * 5 + b], mu[b], s);
+    lam[a] = s;
+  }
+}
 
-  for (int it = cid; it < p.ncells; it += ncl) {
-    const int64_t cell = p.cell_list ? p.cell_list[it] : it;
-    if (t == 0)
-      bulk_load(tbuf, p.tables + (size_t)rank * C::SLAB, kTabBytes, tbar);
-
-    // ---- a3 + a4: gather f* (own j_z planes) and forward FFT in x, y, then z -------------
+// ---- z group: forward z-FFT into TMEM, then z(k) for every direction ----------------------
+template <int N, int P>
+__device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c, uint32_t taddr) {
+  using C = Cfg3<N, P>;
+  constexpr int NP = C::NP, RS = C::RS, GT = C::GT;
+  constexpr int n = N * N * N;
+  constexpr uint32_t kTabBytes = C::SLAB * 16;
+  const int D = p.A + 1;
+  const int rank = c.rank, cid = c.cid, tg = c.tg, tx = c.tx, tl = c.tl;
+  uint32_t tphase = 0;
+  for (int it = cid; it < p.ncells; it += c.ncl) {
+    if (tg == 0) bulk_load(c.tbuf, p.tables + (size_t)rank * C::SLAB, kTabBytes, c.tbar);
+    cluster_sync_all();  // forward xy-FFT of every CTA stored in W[2]
     {
-      constexpr int PER = NP * N * N / C::THREADS;  // = N: elements per thread
-      constexpr int B = PER < 16 ? PER : 16;        // loads in flight per batch
+      double2 x[N];
+      const double2* Wb = c.W + 2 * C::WBUF + (size_t)(rank * NP + tl) * RS + tx;
+#pragma unroll
+      for (int zz = 0; zz < N; ++zz) x[zz] = __ldcg(Wb + (size_t)zz * C::WPLANE);
+      fft<N, -1>(x);
+#pragma unroll
+      for (int ch = 0; ch < N / 8; ++ch) {
+        uint32_t v[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[4 * i + 0] = __double2loint(x[ch * 8 + i].x);
+          v[4 * i + 1] = __double2hiint(x[ch * 8 + i].x);
+          v[4 * i + 2] = __double2loint(x[ch * 8 + i].y);
+          v[4 * i + 3] = __double2hiint(x[ch * 8 + i].y);
+        }
+        tmem_st32(taddr + ch * 32, v);
+      }
+      tmem_wait_st();
+    }
+    {
+      double2 x[N];
+      mbar_wait(c.tbar, tphase);
+      tphase ^= 1;
+      zpass_compute<N, P>(taddr, c.tbuf, tx, tl, x);
+      named_bar(1, GT);  // tbuf consumed
+      if (tg == 0 && D > 1) bulk_load(c.tbuf, p.tables + (size_t)1 * n + (size_t)rank * C::SLAB, kTabBytes, c.tbar);
+      zpass_store<N, P>(x, c.W, rank, tx, tl);  // z(0) -> W[0]
+    }
+#pragma unroll 1
+    for (int k = 0; k <= D + 1; ++k) {
+      // z(k) was stored before this point; computing z(k+1) first lets the release of
+      // arrive(k) find those stores completed (and overlaps the FFT with the barrier).
+      TSTAMP(2048 + k * 8);
+      double2 x[N];
+      const bool more = k + 1 < D;
+      if (more) {
+        mbar_wait(c.tbar, tphase);
+        tphase ^= 1;
+        TSTAMP(2048 + k * 8 + 1);
+        zpass_compute<N, P>(taddr, c.tbuf, tx, tl, x);
+        named_bar(1, GT);  // tbuf consumed
+        if (tg == 0 && k + 2 < D)
+          bulk_load(c.tbuf, p.tables + (size_t)(k + 2) * n + (size_t)rank * C::SLAB, kTabBytes, c.tbar);
+        TSTAMP(2048 + k * 8 + 2);
+      }
+      cl_arrive();  // phase k: z(k) stored (release; the consumers read it through the async proxy
+                    // after their acquire + fence.proxy.async)
+      // W[(k+1)%4] was last read by xy(k-3), finished everywhere before phase k-1 completed.
+      if (more) zpass_store<N, P>(x, c.W + (size_t)((k + 1) % 4) * C::WBUF, rank, tx, tl);
+      TSTAMP(2048 + k * 8 + 3);
+      cl_wait();    // phase k complete
+      TSTAMP(2048 + k * 8 + 4);
+    }
+    if (p.mode == 1) {
+      if (p.project) {
+        double m[5] = {0, 0, 0, 0, 0}, lam[5];
+        project_lambda<N, P>(p, c, false, m, lam);
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+        cl_wait();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- xy group: forward x/y FFT, then xy(k-2) and the gain accumulation, epilogue ------------
+template <int N, int P>
+__device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& c) {
+  using C = Cfg3<N, P>;
+  constexpr int NP = C::NP, RS = C::RS, GT = C::GT;
+  constexpr int n = N * N * N;
+  constexpr uint32_t kPlaneBytes = C::PSLAB * 16;
+  const int D = p.A + 1;
+  const int rank = c.rank, cid = c.cid, tg = c.tg, tx = c.tx, tl = c.tl;
+  uint32_t wphase = 0;  // bit b = parity of plane buffer b
+  for (int it = cid; it < p.ncells; it += c.ncl) {
+    const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    const int z = rank * NP + tl;
+    // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[2]
+    {
+      double2* pln = c.pln0;
+      constexpr int PER = NP * N * N / GT;  // = N elements per thread
+      constexpr int B = PER < 16 ? PER : 16;
 #pragma unroll 1
       for (int b0 = 0; b0 < PER; b0 += B) {
         double v[B];
 #pragma unroll
         for (int j = 0; j < B; ++j) {
-          const int e = t + (b0 + j) * C::THREADS;
-          const int x = e % N, y = (e / N) % N, z = rank * NP + e / (N * N);
-          v[j] = gather_fstar(p.f_in, p.tp, cell, x + N * (y + N * z), x, y, z, n);
+          const int e = tg + (b0 + j) * GT;
+          const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
+          v[j] = gather_fstar(p.f_in, p.tp, cell, x + N * (y + N * zz), x, y, zz, n);
         }
 #pragma unroll
         for (int j = 0; j < B; ++j) {
-          const int e = t + (b0 + j) * C::THREADS;
+          const int e = tg + (b0 + j) * GT;
           const int x = e % N, y = (e / N) % N, zl = e / (N * N);
           pln[zl * N * RS + y * RS + x] = make_double2(v[j], 0.0);
         }
       }
-    }
-    __syncthreads();
-    {
-      double2 r[N];
-      double2* row = pln + tl * N * RS + tx * RS;  // row y = tx of plane tl
-#pragma unroll
-      for (int x = 0; x < N; ++x) r[x] = row[x];
-      fft<N, -1>(r);
-#pragma unroll
-      for (int x = 0; x < N; ++x) row[x] = r[x];
-    }
-    __syncthreads();
-    {
-      double2 c[N];
-      const double2* col = pln + tl * N * RS + tx;  // column l_x = tx of plane tl
-#pragma unroll
-      for (int y = 0; y < N; ++y) c[y] = col[y * RS];
-      fft<N, -1>(c);
-      double2* Wb = Wbase + (size_t)buf * C::WBUF + (size_t)(rank * NP + tl) * C::WPLANE + tx;
-#pragma unroll
-      for (int ly = 0; ly < N; ++ly) Wb[ly * RS] = c[ly];
-    }
-    cluster_sync_all();
-    {
-      double2 c[N];
-      const double2* Wb = Wbase + (size_t)buf * C::WBUF + (size_t)(rank * NP + tl) * RS + tx;
-#pragma unroll
-      for (int z = 0; z < N; ++z) c[z] = __ldcg(Wb + (size_t)z * C::WPLANE);
-      fft<N, -1>(c);
-      double2* fh = fhat + tl * N * N + tx;
-#pragma unroll
-      for (int lz = 0; lz < N; ++lz) fh[lz * N] = c[lz];
-    }
-    buf ^= 1;
-    __syncthreads();  // f^ complete
-
-    // ---- a5/a6: A gain directions + the loss, software-pipelined --------------------------
-    mbar_wait(tbar, tphase);
-    tphase ^= 1;
-    zpass<N, P>(fhat, tbuf, Wbase + (size_t)buf * C::WBUF, rank, tx, tl);
-    __syncthreads();
-    if (t == 0) bulk_load(tbuf, p.tables + (size_t)1 * n + (size_t)rank * C::SLAB, kTabBytes, tbar);
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    cl_arrive();
-
-    double gacc[N];
-#pragma unroll
-    for (int y = 0; y < N; ++y) gacc[y] = 0.0;
-#pragma unroll 1
-    for (int d = 0; d <= p.A; ++d) {
-      const int bd = buf;  // exchange buffer of direction d
-      cl_wait();           // W(d) complete cluster-wide; W(d-1) no longer read anywhere
-      if (t == 0) {
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        bulk_load(pln, Wbase + (size_t)bd * C::WBUF + (size_t)rank * C::PSLAB, kPlaneBytes, wbar);
-      }
-      if (d < p.A) {
-        mbar_wait(tbar, tphase);
-        tphase ^= 1;
-        zpass<N, P>(fhat, tbuf, Wbase + (size_t)(bd ^ 1) * C::WBUF, rank, tx, tl);
-        __syncthreads();  // tbuf consumed
-        if (t == 0 && d + 2 <= p.A)
-          bulk_load(tbuf, p.tables + (size_t)(d + 2) * n + (size_t)rank * C::SLAB, kTabBytes, tbar);
-      }
-      mbar_wait(wbar, wphase);
-      wphase ^= 1;
+      named_bar(2, GT);
       {
         double2 r[N];
-        double2* row = pln + tl * N * RS + tx * RS;
+        double2* row = pln + tl * N * RS + tx * RS;  // row y = tx of plane tl
 #pragma unroll
         for (int x = 0; x < N; ++x) r[x] = row[x];
-        fft<N, +1>(r);
+        fft<N, -1>(r);
 #pragma unroll
         for (int x = 0; x < N; ++x) row[x] = r[x];
       }
-      __syncthreads();
+      named_bar(2, GT);
       {
-        double2 c[N];
-        const double2* col = pln + tl * N * RS + tx;
+        double2 cc[N];
+        const double2* col = pln + tl * N * RS + tx;  // column l_x = tx of plane tl
 #pragma unroll
-        for (int y = 0; y < N; ++y) c[y] = col[y * RS];
-        __syncthreads();  // pln free for the next bulk copy
-        fft<N, +1>(c);
-        if (d < p.A) {
+        for (int y = 0; y < N; ++y) cc[y] = col[y * RS];
+        named_bar(2, GT);  // pln free
+        fft<N, -1>(cc);
+        double2* Wb = c.W + 2 * C::WBUF + (size_t)z * C::WPLANE + tx;
 #pragma unroll
-          for (int y = 0; y < N; ++y) gacc[y] = fma(c[y].x, c[y].y, gacc[y]);
-        } else {
-          const int z = rank * NP + tl;
-          double* g = G + tl * N * N + tx;
-          double fs[N];
-#pragma unroll
-          for (int y = 0; y < N; ++y) fs[y] = gather_fstar(p.f_in, p.tp, cell, tx + N * (y + N * z), tx, y, z, n);
-#pragma unroll
-          for (int y = 0; y < N; ++y) {
-            g[y * N] = gacc[y] - fs[y] * c[y].x;
-            gacc[y] = fs[y];  // gacc now holds the f* column for the Euler update
-          }
-        }
-      }
-      buf ^= 1;
-      if (d < p.A) {
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        cl_arrive();  // z(d+1) stores (issued before xy(d)) are complete by now
+        for (int ly = 0; ly < N; ++ly) Wb[ly * RS] = cc[ly];
       }
     }
-    __syncthreads();
-
-    // ---- a8 + a9: projection and Euler (or write Q) ---------------------------------------
-    const int z = rank * NP + tl;
-    const double* g = G + tl * N * N + tx;
+    cluster_sync_all();
+    double q[N];  // gain accumulator of column (tx, tl), then Q
+#pragma unroll
+    for (int y = 0; y < N; ++y) q[y] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k <= D + 1; ++k) {
+      TSTAMP(k * 8);
+      if (k >= 2) {
+        const int d = k - 2, pb = d & 1;
+        double2* pln = c.pln0 + pb * C::PSLAB;
+        mbar_wait(c.wbar + pb, (wphase >> pb) & 1u);
+        wphase ^= 1u << pb;
+        TSTAMP(k * 8 + 1);
+        // x pass (rows, in place) then y pass (columns, accumulate): one FFT body for both
+        // passes keeps the hot loop's instruction footprint small.
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          double2* vec = pass == 0 ? pln + tl * N * RS + tx * RS : pln + tl * N * RS + tx;
+          const int stride = pass == 0 ? 1 : RS;
+          double2 cc[N];
+#pragma unroll
+          for (int x = 0; x < N; ++x) cc[x] = vec[x * stride];
+          if (pass == 1) named_bar(2, GT);  // plane buffer pb free for the bulk copy of W(k)
+          fft<N, +1>(cc);
+          if (pass == 0) {
+#pragma unroll
+            for (int x = 0; x < N; ++x) vec[x] = cc[x];
+            named_bar(2, GT);
+            TSTAMP(k * 8 + 2);
+          } else if (d < p.A) {
+#pragma unroll
+            for (int y = 0; y < N; ++y) q[y] = fma(cc[y].x, cc[y].y, q[y]);
+          } else {
+#pragma unroll
+            for (int y = 0; y < N; ++y) {
+              const double fs = gather_fstar(p.f_in, p.tp, cell, tx + N * (y + N * z), tx, y, z, n);
+              q[y] = q[y] - fs * cc[y].x;  // Q = G - f* c
+            }
+          }
+        }
+        TSTAMP(k * 8 + 3);
+      }
+      // phase k: xy(k-2) done.  The xy group publishes no global writes (it only read W through
+      // completed bulk copies), so no release fence is needed.
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+      TSTAMP(k * 8 + 4);
+      cl_wait();    // W(k) complete everywhere
+      TSTAMP(k * 8 + 5);
+      if (tg == 0 && k < D) {
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        bulk_load(c.pln0 + (k & 1) * C::PSLAB, c.W + (size_t)(k % 4) * C::WBUF + (size_t)rank * C::PSLAB,
+                  kPlaneBytes, c.wbar + (k & 1));
+      }
+      TSTAMP(k * 8 + 6);
+    }
+    // a8 + a9: projection and Euler (or write Q)
     double* out = p.f_out + cell * (int64_t)n;
     if (p.mode == 0) {
-#pragma unroll 4
-      for (int y = 0; y < N; ++y) out[tx + N * (y + N * z)] = g[y * N];
+#pragma unroll
+      for (int y = 0; y < N; ++y) out[tx + N * (y + N * z)] = q[y];
     } else {
+      const double vx = node_v(tx, p.L, p.dv), vz = node_v(z, p.L, p.dv);
       double lam[5] = {0, 0, 0, 0, 0};
       if (p.project) {
-        const double vx = node_v(tx, p.L, p.dv), vz = node_v(z, p.L, p.dv);
         double m[5] = {0, 0, 0, 0, 0};
+#pragma unroll
         for (int y = 0; y < N; ++y) {
-          const double q = g[y * N], vy = node_v(y, p.L, p.dv);
-          m[0] += q;
-          m[1] += vx * q;
-          m[2] += vy * q;
-          m[3] += vz * q;
-          m[4] += (vx * vx + vy * vy + vz * vz) * q;
+          const double vy = node_v(y, p.L, p.dv);
+          m[0] += q[y];
+          m[1] += vx * q[y];
+          m[2] += vy * q[y];
+          m[3] += vz * q[y];
+          m[4] += (vx * vx + vy * vy + vz * vz) * q[y];
         }
-        constexpr int W = C::THREADS < 32 ? C::THREADS : 32;
-        constexpr unsigned mask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-#pragma unroll
-          for (int o = W / 2; o >= 1; o >>= 1) m[c] += __shfl_xor_sync(mask, m[c], o);
-        }
-        // warps -> CTA partial (fixed order), then the cluster sum through DSMEM in rank order
-        constexpr int NW = (C::THREADS + 31) / 32;
-        double* wpart = reinterpret_cast<double*>(pln);  // scratch: [NW][5]
-        if ((t & 31) == 0) {
-#pragma unroll
-          for (int c = 0; c < 5; ++c) wpart[(t >> 5) * 5 + c] = m[c];
-        }
-        __syncthreads();
-        if (t < 5) {
-          double s = 0.0;
-          for (int w = 0; w < NW; ++w) s += wpart[w * 5 + t];
-          part[t] = s;
-        }
-        cluster_sync_all();
-        double mu[5];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) mu[c] = 0.0;
-        for (int r = 0; r < P; ++r) {
-          const double* rp = cluster.map_shared_rank(part, r);
-#pragma unroll
-          for (int c = 0; c < 5; ++c) mu[c] += rp[c];
-        }
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < 5; ++b) s = fma(p.Ginv[a * 5 + b], mu[b], s);
-          lam[a] = s;
-        }
+        project_lambda<N, P>(p, c, true, m, lam);
       }
-      const double vx = node_v(tx, p.L, p.dv), vz = node_v(z, p.L, p.dv);
       bool bad = false;
 #pragma unroll
       for (int y = 0; y < N; ++y) {
         const double vy = node_v(y, p.L, p.dv);
         const int k = tx + N * (y + N * z);
         const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * vz + lam[4] * (vx * vx + vy * vy + vz * vz);
-        const double o = fma(p.dt_tau, g[y * N] - corr, gacc[y]);
+        const double fs = gather_fstar(p.f_in, p.tp, cell, k, tx, y, z, n);
+        const double o = fma(p.dt_tau, q[y] - corr, fs);
         bad |= !isfinite(o);
         out[k] = o;
       }
@@ -360,8 +450,57 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
         cl_wait();
       }
     }
-    __syncthreads();  // G (= f^ slab) consumed before the next cell's f^
+    __syncthreads();
   }
+}
+
+template <int N, int P>
+__global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepParams p) {
+  using C = Cfg3<N, P>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
+  cg::cluster_group cluster = cg::this_cluster();
+  Ctx3<N, P> c;
+  c.tbuf = reinterpret_cast<double2*>(smem + C::OFF_TBUF);
+  c.pln0 = reinterpret_cast<double2*>(smem + C::OFF_PLN);
+  c.tbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
+  c.wbar = c.tbar + 1;
+  c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
+  c.rank = (int)cluster.block_rank();
+  c.cid = blockIdx.x / P;
+  c.ncl = gridDim.x / P;
+  const int t = threadIdx.x;
+  const bool zg = t < C::GT;
+  c.tg = zg ? t : t - C::GT;
+  c.tx = c.tg % N;
+  c.tl = c.tg / N;
+  c.W = p.scratch + (size_t)c.cid * C::NBUF * C::WBUF;
+
+  if (t < 32) {  // warp 0 owns the TMEM allocation
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (t == 0) {
+    mbar_init(c.tbar, 1);
+    mbar_init(c.wbar, 1);
+    mbar_init(c.wbar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tbase = *tmem_slot;
+  if (zg) {
+    // this thread's TMEM lane: warp quarter base + lane in warp (row field = bits 31..16)
+    z_group<N, P>(p, c, tbase + ((uint32_t)(32 * ((t >> 5) & 3)) << 16));
+  } else {
+    xy_group<N, P>(p, c);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(C::TMEM_COLS) : "memory");
 }
 
 template <int N, int P>
@@ -421,7 +560,7 @@ static int p32() {
 
 cudaError_t launch_step3d(int N, const StepParams& p, int nclusters, cudaStream_t s) {
   switch (N) {
-    case 8: return launch3<8, 8>(p, nclusters, s);
+    case 8: return launch3<8, 2>(p, nclusters, s);
     case 16: return launch3<16, 8>(p, nclusters, s);
     case 32: return p32() == 16 ? launch3<32, 16>(p, nclusters, s) : launch3<32, 8>(p, nclusters, s);
     default: return cudaErrorInvalidValue;
@@ -430,7 +569,7 @@ cudaError_t launch_step3d(int N, const StepParams& p, int nclusters, cudaStream_
 
 int max_active_clusters3d(int N) {
   switch (N) {
-    case 8: return max_clusters3<8, 8>();
+    case 8: return max_clusters3<8, 2>();
     case 16: return max_clusters3<16, 8>();
     case 32: return p32() == 16 ? max_clusters3<32, 16>() : max_clusters3<32, 8>();
     default: return 0;
@@ -438,5 +577,11 @@ int max_active_clusters3d(int N) {
 }
 
 size_t scratch_elems3d(int N) { return (size_t)Cfg3<32, 8>::NBUF * N * N * (N + 1); }
+
+#ifdef FKS_TIMING
+extern "C" int fks_debug_tstamps(long long* out, int count) {
+  return (int)cudaMemcpyFromSymbol(out, g_tstamp, sizeof(long long) * count);
+}
+#endif
 
 }  // namespace fks

@@ -1,0 +1,25 @@
+"""Read the per-phase clock64 stamps of cluster 0 / CTA 0 (build with FKS_TIMING=1)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import workloads
+from paper_1608_08009_b200 import fks, _lib
+c = workloads.config("C2")
+N, L = c["N"], c["L"]
+nc = 256
+f = workloads.initial_state(c, ncells=64)
+F = np.concatenate([f] * 4)
+ctx = fks.Context(3, 0, [nc], N, L, 24)
+a = torch.from_numpy(F).cuda(); b = torch.empty_like(a)
+ctx.step(a, b, c["dt"]); torch.cuda.synchronize()
+ctx.step(b, a, c["dt"]); torch.cuda.synchronize()
+buf = (ctypes.c_longlong * 4096)()
+_lib.load().fks_debug_tstamps(buf, 4096)
+ts = np.array(buf[:])
+base = ts[2 * 8]
+def r(v): return v - base if v else -1
+print("k | xy: top  Wland  xdone  ydone  arrive  waitret  issued | z: arrive Tland zcomp waitret stored")
+for k in range(27):
+    xy = [r(v) for v in ts[k*8:k*8+7]]
+    z = [r(v) for v in ts[2048+k*8:2048+k*8+5]]
+    print(k, "|", " ".join(f"{v:7d}" for v in xy), "|", " ".join(f"{v:7d}" for v in z))
