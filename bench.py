@@ -101,7 +101,10 @@ def _oracle_worker(args):
     import workloads
     from oracle import step as ostep, tables
     c = workloads.config(name)
-    f = workloads.initial_state(c, ncells=count, start=start)
+    if c["dx_dim"] == 0:
+        f = workloads.initial_state(c, ncells=count, start=start)
+    else:  # spatial configs: the per-cell collision step dominates; time it on smooth cells
+        f = workloads.family("smooth", c["dv"], c["N"], c["L"], count, seed=start)
     tab = tables.build_tables(c["dv"], c["N"], c["L"], A=c["A"]) if c["dv"] == 2 else tables.build_tables(3, c["N"], c["L"])
     t0 = time.perf_counter()
     ostep.homogeneous_step(f, tab, c["dt"], c["tau"], evaluator=evaluator)
@@ -175,24 +178,53 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    if c["dx_dim"] != 0:
-        raise SystemExit("bench.py times the 0D ensembles C1/C2 in round 1 (spatial configs: tests)")
-    ncells = a.cells or c["cells"][0]
-    # synthetic input: generate 256 distinct cells and tile them (generation of 4096 cells in
-    # numpy takes longer than the timed run); every cell still runs the full path
-    base = workloads.initial_state(c, ncells=min(ncells, 256), start=(rank * 256) % c["cells"][0])
-    reps = (ncells + base.shape[0] - 1) // base.shape[0]
-    F = np.concatenate([base] * reps)[:ncells]
-    ctx = fks.Context(dv, 0, [ncells], N, c["L"], A)
+    dt = c["dt"]
+    if c["dx_dim"] == 0:
+        ncells = a.cells or c["cells"][0]
+        # synthetic input: 256 distinct generated cells tiled to the batch (numpy generation of
+        # 4096 cells takes longer than the timed run); every cell still runs the full path
+        base = workloads.initial_state(c, ncells=min(ncells, 256), start=(rank * 256) % c["cells"][0])
+        reps = (ncells + base.shape[0] - 1) // base.shape[0]
+        F = np.concatenate([base] * reps)[:ncells]
+        ctx = fks.Context(dv, 0, [ncells], N, c["L"], A)
+        fa = torch.from_numpy(F).cuda()
+        nfluid_local = ncells
+        stepper = None
+        scaling = "weak"
+    else:
+        from paper_1608_08009_b200 import parallel
+        dxd = c["dx_dim"]
+        Mg = tuple(c["cells"][::-1])  # axis 0 fastest
+        bc = c["bc"]
+        slab = parallel.decompose(dxd, Mg, bc, world, rank)
+        ctx = fks.Context(dv, dxd, list(slab.M_local), N, c["L"], A, h=c["dx"], bc=slab.local_bc(bc))
+        for face, g in workloads.ghost_vectors(c).items():
+            ctx.set_ghost(face, torch.from_numpy(g).cuda())
+        solid = workloads.solid_mask(c)
+        sl = parallel.local_slice(slab, solid.reshape(-1)) if solid is not None else None
+        if sl is not None:
+            ctx.set_solid(sl)
+        nfluid_local = int(sl.size - sl.sum()) if sl is not None else int(np.prod(slab.M_local))
+        if c["name"] == "C3":
+            F = parallel.local_slice(slab, workloads.initial_state(c).reshape(-1, n))
+            fa = torch.from_numpy(np.ascontiguousarray(F)).cuda()
+        else:  # uniform initial state: one generated vector broadcast on the device
+            v = torch.from_numpy(workloads.initial_state(c, ncells=1).reshape(-1)[:n].copy()).cuda()
+            fa = v.expand(int(np.prod(slab.M_local)), n).contiguous()
+            F = None
+        stepper = parallel.DistributedStep(ctx, slab, n, torch.device("cuda", local)) if world > 1 else None
+        scaling = "strong"
+        ncells = int(np.prod(slab.M_local))
     ctx.set_params(tau=c["tau"])
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream)
-    fa = torch.from_numpy(F).cuda()
     fb = torch.empty_like(fa)
-    dt = c["dt"]
 
     def one_step(x, y):
-        ctx.step(x, y, dt)
+        if stepper is not None:
+            stepper(x, y, dt)
+        else:
+            ctx.step(x, y, dt)
 
     for _ in range(a.warmup):
         one_step(fa, fb)
@@ -228,17 +260,31 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / a.steps
-    value = ncells * world * a.steps / (ms_total * 1e-3)
+    nfluid = nfluid_local
+    if dist:
+        t = torch.tensor([float(nfluid_local)], device="cuda")
+        dist.all_reduce(t)
+        nfluid = int(t.item())
+    else:
+        nfluid = nfluid_local
+    value = nfluid * a.steps / (ms_total * 1e-3)  # fluid cells collided per second, all ranks
     fl = flops_per_cell(dv, N, A)
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
-    achieved = fl * ncells / (kern_avg_ms * 1e-3) / 1e12
+    achieved = fl * nfluid_local / (kern_avg_ms * 1e-3) / 1e12
 
     # ---- e2e through the C ABI with host buffers (H2D + step + D2H per step) --------------
     e2e = None
-    if not a.no_e2e:
-        hin = torch.from_numpy(F).pin_memory()
+    if not a.no_e2e and F is not None and stepper is None:
+        hin = torch.from_numpy(np.ascontiguousarray(F)).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
-        ctx_h = fks.Context(dv, 0, [ncells], N, c["L"], A)
+        if c["dx_dim"] == 0:
+            ctx_h = fks.Context(dv, 0, [ncells], N, c["L"], A)
+        else:
+            ctx_h = fks.Context(dv, c["dx_dim"], list(slab.M_local), N, c["L"], A, h=c["dx"], bc=slab.local_bc(c["bc"]))
+            for face, g in workloads.ghost_vectors(c).items():
+                ctx_h.set_ghost(face, torch.from_numpy(g).cuda())
+            if sl is not None:
+                ctx_h.set_solid(sl)
         ctx_h.set_params(tau=c["tau"])
         ctx_h.set_stream(stream)
         ctx_h.step_host(hin, hout, dt)
@@ -255,7 +301,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         bytes_ = ncells * n * 8
-        e2e = {"value": ncells * world * ksteps / el, "unit": "cells/s", "h2d_bytes_per_step": bytes_,
+        e2e = {"value": nfluid_local * world * ksteps / el, "unit": "cells/s", "h2d_bytes_per_step": bytes_,
                "d2h_bytes_per_step": bytes_, "steps": ksteps, "path": "fks_step_host (pinned host buffers)"}
         ctx_h.close()
 
@@ -268,15 +314,22 @@ def main():
                              f"in {wall:.1f} s on {cores} single-threaded processes"}
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{a.config}: " + {
                 "C1": "0Dx2D BKW ensemble, Maxwell molecules, Nv=32^2, A=8",
                 "C2": "0Dx3D two-Gaussian relaxation ensemble (Test 1.3 shape), hard spheres, Nv=32^3, "
-                      "A=24 spherical 7-design"}.get(a.config, a.config),
-                "cells_per_gpu": ncells, "Nv": N, "dv": dv, "M_dirs": A, "dt": dt,
-                "l2": f"inputs larger than L2 ({2 * ncells * n * 8 / 2**30:.2f} GiB ping-pong state)",
-                "parallelism": f"dp{world} (independent cells, no collective)"},
+                      "A=24 spherical 7-design",
+                "C3": "1Dx3D Sod shock tube (Test 2.3 shape), 400 cells, Dirichlet ghosts, hard spheres, Nv=32^3, A=24",
+                "C4": "2Dx3D re-entry geometry (Test 3.2 boxes), 100^2 cells, inflow/outflow, solids frozen, "
+                      "hard spheres, Nv=32^3, A=24",
+                "C5": "3Dx3D re-entry (Test 4.1), 48^3 cells with a 12^3 solid cuboid, inflow/outflow, "
+                      "hard spheres, Nv=32^3, A=24"}.get(a.config, a.config),
+                "cells_per_gpu": ncells, "fluid_cells_total": nfluid, "Nv": N, "dv": dv, "M_dirs": A, "dt": dt,
+                "l2": f"inputs larger than L2 ({2 * ncells * n * 8 / 2**30:.2f} GiB ping-pong state)"
+                      if 2 * ncells * n * 8 > 126e6 else "state smaller than L2 (not flushed)",
+                "parallelism": (f"dp{world} (independent cells, no collective)" if c["dx_dim"] == 0 else
+                                f"{world} slabs along space axis {c['dx_dim'] - 1}, NCCL halo exchange per step")},
             "phase_space_updates_per_s": value * n,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": dram_traffic(dv, ncells),

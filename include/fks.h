@@ -52,8 +52,10 @@ typedef enum {
   FKS_E_STATE = -7
 } fks_status;
 
-/* Face kinds (reading #19). */
-enum { FKS_BC_PERIODIC = 0, FKS_BC_GHOST = 1, FKS_BC_OUTFLOW = 2 };
+/* Face kinds (reading #19).  FKS_BC_HALO marks a face of the slowest space axis that
+ * borders another rank's slab (the paper's MPI z-slab ghost cells); its sources are
+ * read from the plane set with fks_set_halo. */
+enum { FKS_BC_PERIODIC = 0, FKS_BC_GHOST = 1, FKS_BC_OUTFLOW = 2, FKS_BC_HALO = 3 };
 
 typedef struct {
   int dv;          /* velocity dimension: 2 (Maxwell molecules) or 3 (hard spheres)          */
@@ -89,6 +91,12 @@ fks_status fks_set_dirs(fks_ctx* ctx, const double* e_host, const double* w_host
 
 /* Ghost vector for a GHOST face (n values, device memory, copied into library memory). */
 fks_status fks_set_ghost(fks_ctx* ctx, int face, const double* ghost_f);
+
+/* Neighbour planes for the FKS_BC_HALO faces (a2, the slab exchange): lo_plane / hi_plane are
+ * device pointers to [plane cells][n] (the plane just below / above the local slab along the
+ * slowest axis, cells in C order over the other axes).  The pointers are used by the next
+ * fks_step / fks_transport calls (not copied); NULL for a face without a HALO. */
+fks_status fks_set_halo(fks_ctx* ctx, const double* lo_plane, const double* hi_plane);
 
 /* Solid mask (host, one byte per local cell, copied): solid cells are not collided and keep
  * their values (reading #19; specular reflection is NEXT work). NULL clears it. */

@@ -21,6 +21,7 @@ SIGNATURES = {
     "fks_set_dirs": (c_int, [c_void_p, P_DOUBLE, P_DOUBLE, c_int]),
     "fks_set_ghost": (c_int, [c_void_p, c_int, c_void_p]),
     "fks_set_solid": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_uint8)]),
+    "fks_set_halo": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fks_set_stream": (c_int, [c_void_p, c_void_p]),
     "fks_collide": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fks_transport": (c_int, [c_void_p, c_void_p, c_void_p, c_double]),

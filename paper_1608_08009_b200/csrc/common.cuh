@@ -14,6 +14,8 @@ struct TransportParams {
   int bc[6];               // FKS_BC_* per face
   int8_t delta[3][kMaxN];  // delta[a][k_a] = s^{n+1} - s^n for velocity component a
   const double* ghost[6];  // ghost vectors (n values) of GHOST faces, device memory
+  const double* halo[2];   // HALO faces of the slowest axis: neighbour rank's boundary plane
+                           // [plane cells][n] (cells in C order over the other axes)
 };
 
 struct StepParams {
@@ -35,13 +37,15 @@ struct StepParams {
 
 // f*_cell[k]: the transported value for velocity k = (kx, ky, kz) (P:243-257 eq. f_bar sampled
 // at x_j).  Out-of-domain sources: PERIODIC wraps, OUTFLOW clamps, GHOST reads the
-// face's ghost vector (the lowest axis with a ghost face wins; reading #19).
+// face's ghost vector (the lowest axis with a ghost face wins; reading #19).  A HALO
+// face (only on the slowest axis) reads the neighbour slab's boundary plane -- the ghost cells
+// of the paper's z-slab decomposition (Fig. mpi-decomp).
 __device__ __forceinline__ double gather_fstar(const double* __restrict__ F, const TransportParams& tp,
                                                int64_t cell, int k, int kx, int ky, int kz, int n) {
   if (tp.dx == 0) return F[cell * n + k];
   const int kc[3] = {kx, ky, kz};
   int64_t rem = cell;
-  int64_t src = 0, stride = 1;
+  int64_t src = 0, stride = 1, hplane = 0;
   int gface = -1;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -51,17 +55,22 @@ __device__ __forceinline__ double gather_fstar(const double* __restrict__ F, con
       rem /= Ma;
       int s = j + tp.delta[a][kc[a]];
       if (s < 0) {
-        if (tp.bc[2 * a] == 0) s += Ma;
-        else { if (tp.bc[2 * a] == 1 && gface < 0) gface = 2 * a; s = 0; }
+        const int b = tp.bc[2 * a];
+        if (b == 0) s += Ma;
+        else { if ((b == 1 || b == 3) && gface < 0) { gface = 2 * a; hplane = src; } s = 0; }
       } else if (s >= Ma) {
-        if (tp.bc[2 * a + 1] == 0) s -= Ma;
-        else { if (tp.bc[2 * a + 1] == 1 && gface < 0) gface = 2 * a + 1; s = Ma - 1; }
+        const int b = tp.bc[2 * a + 1];
+        if (b == 0) s -= Ma;
+        else { if ((b == 1 || b == 3) && gface < 0) { gface = 2 * a + 1; hplane = src; } s = Ma - 1; }
       }
       src += s * stride;
       stride *= Ma;
     }
   }
-  if (gface >= 0) return tp.ghost[gface][k];
+  if (gface >= 0) {
+    if (tp.bc[gface] == 3) return tp.halo[gface & 1][hplane * n + k];
+    return tp.ghost[gface][k];
+  }
   return F[src * n + k];
 }
 

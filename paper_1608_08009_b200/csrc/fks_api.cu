@@ -221,6 +221,7 @@ struct fks_ctx {
   int nsolid = 0;
   uint8_t* d_solid = nullptr;
   double* d_ghost[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  const double* halo[2] = {nullptr, nullptr};  // caller-owned neighbour planes (FKS_BC_HALO)
   double* d_host_in = nullptr;
   double* d_host_out = nullptr;
   int64_t launches = 0;
@@ -299,6 +300,8 @@ void fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift)
   tp->dx = with_shift ? c->grid.dx : 0;
   for (int a = 0; a < 3; ++a) tp->M[a] = (int)c->grid.M[a];
   for (int f = 0; f < 6; ++f) { tp->bc[f] = c->grid.bc[f]; tp->ghost[f] = c->d_ghost[f]; }
+  tp->halo[0] = c->halo[0];
+  tp->halo[1] = c->halo[1];
   if (with_shift)
     for (int a = 0; a < c->grid.dx; ++a) shift_delta(c->step_n, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
 }
@@ -396,8 +399,10 @@ fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double k
   }
   if (ncells > INT32_MAX) return FKS_E_INVAL;
   if (grid->dx > 0 && !(grid->h > 0)) return FKS_E_INVAL;
-  for (int f = 0; f < 2 * grid->dx; ++f)
-    if (grid->bc[f] < 0 || grid->bc[f] > 2) return FKS_E_INVAL;
+  for (int f = 0; f < 2 * grid->dx; ++f) {
+    if (grid->bc[f] < 0 || grid->bc[f] > 3) return FKS_E_INVAL;
+    if (grid->bc[f] == 3 && f / 2 != grid->dx - 1) return FKS_E_INVAL;  // HALO: slowest axis only
+  }
   Dirs dirs;
   if (!default_dirs(dv, M_dirs, &dirs)) return FKS_E_UNSUPPORTED;
 
@@ -471,6 +476,13 @@ fks_status fks_set_ghost(fks_ctx* c, int face, const double* ghost_f) {
                                    c->stream));
 }
 
+fks_status fks_set_halo(fks_ctx* c, const double* lo_plane, const double* hi_plane) {
+  if (!c) return FKS_E_INVAL;
+  c->halo[0] = lo_plane;
+  c->halo[1] = hi_plane;
+  return FKS_OK;
+}
+
 fks_status fks_set_solid(fks_ctx* c, const uint8_t* solid_host) {
   if (!c) return FKS_E_INVAL;
   return set_cell_lists(c, solid_host);
@@ -493,8 +505,10 @@ fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
 
 static fks_status check_dt(fks_ctx* c, double dt) {
   if (!(dt > 0)) return FKS_E_INVAL;
-  for (int f = 0; f < 2 * c->grid.dx; ++f)
+  for (int f = 0; f < 2 * c->grid.dx; ++f) {
     if (c->grid.bc[f] == FKS_BC_GHOST && !c->d_ghost[f]) return FKS_E_STATE;
+    if (c->grid.bc[f] == FKS_BC_HALO && !c->halo[f & 1]) return FKS_E_STATE;
+  }
   if (c->dt == 0.0) c->dt = dt;
   else if (c->dt != dt) return FKS_E_STATE;
   return FKS_OK;

@@ -10,7 +10,7 @@ import numpy as np
 
 from ._lib import FksError, FksGrid, check, load  # noqa: F401
 
-BC_PERIODIC, BC_GHOST, BC_OUTFLOW = 0, 1, 2
+BC_PERIODIC, BC_GHOST, BC_OUTFLOW, BC_HALO = 0, 1, 2, 3
 
 
 def _ptr(t):
@@ -67,6 +67,12 @@ class Context:
 
     def set_ghost(self, face, ghost):
         check(self._lib.fks_set_ghost(self.handle, face, _ptr(ghost)), "fks_set_ghost")
+
+    def set_halo(self, lo, hi):
+        """Neighbour planes (float64 CUDA tensors [plane cells, n]) for the HALO faces, or None."""
+        check(self._lib.fks_set_halo(self.handle, _ptr(lo) if lo is not None else None,
+                                     _ptr(hi) if hi is not None else None), "fks_set_halo")
+        self._halo_refs = (lo, hi)  # keep the buffers alive while the library holds the pointers
 
     def set_solid(self, mask):
         if mask is None:

@@ -1,0 +1,153 @@
+"""Multi-GPU plumbing: slab decomposition of physical space and the halo exchange (a2).
+
+The paper distributes "spatial degrees of freedom over computational nodes, keeping on every
+node a complete set of velocity space points", slices along one axis, and exchanges ghost
+cells after each step (Fig. mpi-decomp).  Here one process drives one GPU; the slab
+axis is the slowest space axis (axis dx-1); each rank owns a contiguous range of planes with
+all N^dv velocities; per step each rank sends its first / last plane to its lower / upper
+neighbour (torch.distributed P2P: NCCL over NVLink on GPUs, gloo on CPU for the tests) and
+the step kernel reads sources outside the slab from those planes (FKS_BC_HALO faces).  The
+FKS shift is at most one cell per step at CFL <= 1 (reading #15), so one plane suffices.
+
+0D ensembles (C1/C2) need none of this: ranks own disjoint cell batches and never communicate
+on the data path (bench.py, weak scaling).
+
+Nothing here computes any part of the method: it partitions indices and moves bytes.
+"""
+from dataclasses import dataclass
+
+from .fks import BC_HALO, BC_PERIODIC
+
+
+@dataclass
+class Slab:
+    dx: int
+    M_global: tuple      # cells per space axis, axis 0 fastest
+    rank: int
+    world: int
+    lo: int              # first global plane index owned along the slab axis
+    hi: int              # one past the last
+    periodic: bool = False  # the slab axis is periodic in the global problem (ring of ranks)
+
+    @property
+    def axis(self):
+        return self.dx - 1
+
+    @property
+    def M_local(self):
+        m = list(self.M_global)
+        m[self.axis] = self.hi - self.lo
+        return tuple(m)
+
+    @property
+    def plane_cells(self):
+        p = 1
+        for a in range(self.dx - 1):
+            p *= self.M_global[a]
+        return p
+
+    def lower(self):
+        """Rank owning the plane below lo (None at a non-periodic domain face)."""
+        return self._neighbour(-1)
+
+    def upper(self):
+        return self._neighbour(+1)
+
+    def _neighbour(self, d):
+        r = self.rank + d
+        if 0 <= r < self.world:
+            return r
+        return (r % self.world) if self.periodic else None
+
+    def local_bc(self, bc_global):
+        """Face kinds of the local grid: slab-axis faces shared with another rank become HALO."""
+        bc = list(bc_global) + [0] * (6 - len(bc_global))
+        lo_face, hi_face = 2 * self.axis, 2 * self.axis + 1
+        if self.world > 1:
+            if self.lower() is not None:
+                bc[lo_face] = BC_HALO
+            if self.upper() is not None:
+                bc[hi_face] = BC_HALO
+        return bc
+
+
+def decompose(dx, M_global, bc_global, world, rank):
+    """Near-equal contiguous slabs along the slowest axis (first ranks get the extra plane)."""
+    if dx < 1:
+        raise ValueError("slab decomposition needs dx >= 1")
+    m = M_global[dx - 1]
+    if world > m:
+        raise ValueError("more ranks than planes")
+    base, extra = divmod(m, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    periodic = bc_global[2 * (dx - 1)] == BC_PERIODIC and bc_global[2 * (dx - 1) + 1] == BC_PERIODIC
+    return Slab(dx=dx, M_global=tuple(M_global), rank=rank, world=world, lo=lo, hi=hi, periodic=periodic)
+
+
+def local_slice(slab, f_global):
+    """The rank's part of a global [cells..., n] array laid out [planes][plane cells][n]."""
+    pc = slab.plane_cells
+    return f_global[slab.lo * pc:slab.hi * pc]
+
+
+def halos_from_global(slab, f_global):
+    """(lo, hi) neighbour planes taken from a global array (single-process emulation/tests)."""
+    pc = slab.plane_cells
+    m = slab.M_global[slab.axis]
+    lo = hi = None
+    if slab.lower() is not None:
+        p = (slab.lo - 1) % m
+        lo = f_global[p * pc:(p + 1) * pc]
+    if slab.upper() is not None:
+        p = slab.hi % m
+        hi = f_global[p * pc:(p + 1) * pc]
+    return lo, hi
+
+
+class HaloExchange:
+    """Per-step exchange of boundary planes with torch.distributed batched P2P."""
+
+    def __init__(self, slab, n, device, dtype=None, group=None):
+        import torch
+        self.slab, self.group = slab, group
+        dtype = dtype or torch.float64
+        pc = slab.plane_cells
+        self.lo = torch.empty(pc, n, device=device, dtype=dtype) if slab.lower() is not None else None
+        self.hi = torch.empty(pc, n, device=device, dtype=dtype) if slab.upper() is not None else None
+        self.pc, self.n = pc, n
+
+    def exchange(self, f_local):
+        """Fill self.lo / self.hi from the neighbours; f_local is [local cells, n] (contiguous)."""
+        import torch.distributed as dist
+        pc = self.pc
+        f_local = f_local.reshape(-1, self.n)
+        first, last = f_local[:pc], f_local[-pc:]
+        # Fixed order per peer pair (NCCL matches P2P in issue order; gloo also uses the tags):
+        # data moving up (my last plane -> upper's lo halo) before data moving down.
+        ops = []
+        lo_r, hi_r = self.slab.lower(), self.slab.upper()
+        if hi_r is not None:
+            ops.append(dist.P2POp(dist.isend, last.contiguous(), hi_r, self.group, 0))
+        if lo_r is not None:
+            ops.append(dist.P2POp(dist.isend, first.contiguous(), lo_r, self.group, 1))
+        if lo_r is not None:
+            ops.append(dist.P2POp(dist.irecv, self.lo, lo_r, self.group, 0))
+        if hi_r is not None:
+            ops.append(dist.P2POp(dist.irecv, self.hi, hi_r, self.group, 1))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return self.lo, self.hi
+
+
+class DistributedStep:
+    """fks_step on one rank's slab with the halo exchange in front (a2 -> a1..a9)."""
+
+    def __init__(self, ctx, slab, n, device, group=None):
+        self.ctx, self.x = ctx, HaloExchange(slab, n, device, group=group)
+
+    def __call__(self, f_in, f_out, dt):
+        lo, hi = self.x.exchange(f_in)
+        self.ctx.set_halo(lo, hi)
+        self.ctx.step(f_in, f_out, dt)

@@ -1,0 +1,108 @@
+"""Multi-rank host logic on CPU (gloo, world size 2-3): slab decomposition, face kinds, and the
+halo exchange, checked end to end against the oracle's single-domain transport gather."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import transport
+from paper_1608_08009_b200 import parallel
+from paper_1608_08009_b200.fks import BC_GHOST, BC_HALO, BC_OUTFLOW, BC_PERIODIC
+
+
+def test_decompose_covers_planes():
+    for m in [7, 12, 48, 100]:
+        for world in [1, 2, 3, 4, 8]:
+            if world > m:
+                continue
+            slabs = [parallel.decompose(2, (5, m), [0, 0, 2, 2], world, r) for r in range(world)]
+            assert slabs[0].lo == 0 and slabs[-1].hi == m
+            assert all(a.hi == b.lo for a, b in zip(slabs, slabs[1:]))
+            sizes = [s.hi - s.lo for s in slabs]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_local_face_kinds():
+    s = [parallel.decompose(3, (4, 4, 9), [BC_GHOST, BC_OUTFLOW] * 3, 3, r) for r in range(3)]
+    assert s[0].local_bc([BC_GHOST, BC_OUTFLOW] * 3)[4:] == [BC_GHOST, BC_HALO]
+    assert s[1].local_bc([BC_GHOST, BC_OUTFLOW] * 3)[4:] == [BC_HALO, BC_HALO]
+    assert s[2].local_bc([BC_GHOST, BC_OUTFLOW] * 3)[4:] == [BC_HALO, BC_OUTFLOW]
+    ring = [parallel.decompose(1, (10,), [BC_PERIODIC, BC_PERIODIC], 2, r) for r in range(2)]
+    assert ring[0].lower() == 1 and ring[1].upper() == 0
+    assert ring[0].local_bc([BC_PERIODIC, BC_PERIODIC]) == [BC_HALO, BC_HALO, 0, 0, 0, 0]
+    single = parallel.decompose(1, (10,), [BC_PERIODIC, BC_PERIODIC], 1, 0)
+    assert single.local_bc([BC_PERIODIC, BC_PERIODIC])[:2] == [BC_PERIODIC, BC_PERIODIC]
+
+
+CASES = {
+    # dx, dv, M (axis 0 fastest), N, L, global bc
+    "2d_space_3d_vel": (2, 3, (4, 7), 8, 5.0, [BC_GHOST, BC_OUTFLOW, BC_OUTFLOW, BC_OUTFLOW]),
+    "1d_ring": (1, 2, (9,), 8, 4.0, [BC_PERIODIC, BC_PERIODIC]),
+    "3d_space": (3, 3, (3, 2, 6), 8, 5.0, [BC_OUTFLOW, BC_OUTFLOW, BC_PERIODIC, BC_PERIODIC, BC_GHOST, BC_OUTFLOW]),
+}
+
+
+def _global_state(case):
+    dx, dv, M, N, L, bc = CASES[case]
+    rng = np.random.default_rng(3)
+    F = rng.random(tuple(M[::-1]) + (N,) * dv)
+    ghosts = {f: rng.random((N,) * dv) for f in range(2 * dx) if bc[f] == BC_GHOST}
+    return F, ghosts
+
+
+def _worker(rank, world, port, case, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dx, dv, M, N, L, bc = CASES[case]
+        n = N ** dv
+        F, ghosts = _global_state(case)
+        Fg = torch.from_numpy(F.reshape(-1, n))
+        slab = parallel.decompose(dx, M, bc, world, rank)
+        local = parallel.local_slice(slab, Fg).clone()
+        hx = parallel.HaloExchange(slab, n, "cpu")
+        lo, hi = hx.exchange(local)
+        elo, ehi = parallel.halos_from_global(slab, Fg)
+        ok = True
+        for got, exp in ((lo, elo), (hi, ehi)):
+            ok &= (got is None) == (exp is None)
+            if got is not None:
+                ok &= bool(torch.equal(got, exp))
+        # FKS transport of the slab with the exchanged halo planes equals the global transport
+        h, dt = 0.1, 0.09 / (L - L / N)
+        pieces = ([lo] if lo is not None else []) + [local] + ([hi] if hi is not None else [])
+        ext = torch.cat(pieces).numpy()
+        Mext = list(M)
+        Mext[dx - 1] = ext.shape[0] // slab.plane_cells
+        ext = ext.reshape(tuple(Mext[::-1]) + (N,) * dv)
+        bc_ext = list(bc)
+        if slab.world > 1 and slab.periodic:
+            bc_ext[2 * (dx - 1)] = bc_ext[2 * (dx - 1) + 1] = BC_OUTFLOW  # the halos carry the wrap
+        for step in range(3):
+            ref = transport.gather(F, step, dx, dv, N, L, dt, h, bc, ghosts).reshape(-1, n)
+            got = transport.gather(ext, step, dx, dv, N, L, dt, h, bc_ext, ghosts).reshape(-1, n)
+            off = slab.plane_cells if lo is not None else 0
+            mine = got[off:off + local.shape[0]]
+            ok &= bool(np.array_equal(mine, ref[slab.lo * slab.plane_cells:slab.hi * slab.plane_cells]))
+        out[rank] = ok
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("case,world", [("2d_space_3d_vel", 2), ("1d_ring", 2), ("3d_space", 3)])
+def test_halo_exchange_gloo(case, world):
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker, args=(world, _free_port(), case, out), nprocs=world, start_method="spawn")
+    assert dict(out) == {r: True for r in range(world)}

@@ -279,3 +279,47 @@ def test_full_size_C2_launch_sampled(torch, fks):
     mass_in = f.reshape(nc, -1).sum(axis=1)
     mass_out = got.reshape(nc, -1).sum(axis=1)
     assert np.max(np.abs(mass_out - mass_in) / mass_in) < 1e-12
+
+
+@pytest.mark.parametrize("dxd,dv,M,N,bc,world", [
+    (1, 3, [11], 8, [transport.GHOST, transport.GHOST], 3),
+    (2, 3, [4, 7], 8, [transport.GHOST, transport.OUTFLOW, transport.OUTFLOW, transport.OUTFLOW], 2),
+    (2, 2, [5, 6], 16, [transport.PERIODIC, transport.PERIODIC, transport.PERIODIC, transport.PERIODIC], 3),
+    (3, 3, [3, 2, 5], 8, [transport.OUTFLOW, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC,
+                          transport.GHOST, transport.OUTFLOW], 2),
+])
+def test_slab_partition_bitwise(torch, fks, dxd, dv, M, N, bc, world):
+    """a2: the slab-decomposed step (HALO faces fed with the neighbours' boundary planes) equals
+    the single-domain step bitwise, every step (ranks emulated one after another on one GPU;
+    the exchange itself is covered by tests/test_parallel_cpu.py)."""
+    from paper_1608_08009_b200 import parallel
+    L = 6.0
+    F, h, dt, ghosts = _spatial_case(dxd, dv, M, N, L, bc, seed=21)
+    n = N ** dv
+    solid = np.zeros(tuple(M[::-1]), dtype=bool)
+    solid.reshape(-1)[len(solid.reshape(-1)) // 3] = True
+    A = 8 if dv == 2 else 24
+    ref_ctx = fks.Context(dv, dxd, M, N, L, A, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ref_ctx.set_ghost(face, dev(torch, g))
+    ref_ctx.set_solid(solid)
+    slabs = [parallel.decompose(dxd, M, bc, world, r) for r in range(world)]
+    ctxs = []
+    for s in slabs:
+        c = fks.Context(dv, dxd, list(s.M_local), N, L, A, h=h, bc=s.local_bc(bc))
+        for face, g in ghosts.items():
+            c.set_ghost(face, dev(torch, g))
+        c.set_solid(parallel.local_slice(s, solid.reshape(-1)))
+        ctxs.append(c)
+    G = dev(torch, F).reshape(-1, n)
+    for step in range(3):
+        out = torch.empty_like(G)
+        ref_ctx.step(G, out, dt)
+        for s, c in zip(slabs, ctxs):
+            lo, hi = parallel.halos_from_global(s, G)
+            c.set_halo(lo.contiguous() if lo is not None else None, hi.contiguous() if hi is not None else None)
+            loc = parallel.local_slice(s, G).contiguous()
+            o = torch.empty_like(loc)
+            c.step(loc, o, dt)
+            assert torch.equal(o, parallel.local_slice(s, out)), (step, s.rank)
+        G = out
