@@ -35,25 +35,47 @@ struct StepParams {
   TransportParams tp;
 };
 
+// Coordinates of a local cell along each space axis (computed once per cell, not per element).
+struct CellCoord {
+  int j[3];
+  int64_t cell;
+};
+
+__device__ __forceinline__ CellCoord cell_coord(const TransportParams& tp, int64_t cell) {
+  CellCoord c;
+  c.cell = cell;
+  int64_t rem = cell;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a < tp.dx) {
+      c.j[a] = (int)(rem % tp.M[a]);
+      rem /= tp.M[a];
+    } else {
+      c.j[a] = 0;
+    }
+  }
+  return c;
+}
+
 // f*_cell[k]: the transported value for velocity k = (kx, ky, kz) (P:243-257 eq. f_bar sampled
 // at x_j).  Out-of-domain sources: PERIODIC wraps, OUTFLOW clamps, GHOST reads the
 // face's ghost vector (the lowest axis with a ghost face wins; reading #19).  A HALO
 // face (only on the slowest axis) reads the neighbour slab's boundary plane -- the ghost cells
 // of the paper's z-slab decomposition (Fig. mpi-decomp).
+// delta: the shift table [3][kMaxN] (a shared-memory copy of tp.delta in the hot kernels: its
+// index varies across a warp, which serialises constant-bank loads).
 __device__ __forceinline__ double gather_fstar(const double* __restrict__ F, const TransportParams& tp,
-                                               int64_t cell, int k, int kx, int ky, int kz, int n) {
-  if (tp.dx == 0) return F[cell * n + k];
+                                               const CellCoord& cc, int k, int kx, int ky, int kz, int n,
+                                               const int8_t (*delta)[kMaxN]) {
+  if (tp.dx == 0) return F[cc.cell * n + k];
   const int kc[3] = {kx, ky, kz};
-  int64_t rem = cell;
   int64_t src = 0, stride = 1, hplane = 0;
   int gface = -1;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     if (a < tp.dx) {
       const int Ma = tp.M[a];
-      const int j = (int)(rem % Ma);
-      rem /= Ma;
-      int s = j + tp.delta[a][kc[a]];
+      int s = cc.j[a] + delta[a][kc[a]];
       if (s < 0) {
         const int b = tp.bc[2 * a];
         if (b == 0) s += Ma;
@@ -72,6 +94,11 @@ __device__ __forceinline__ double gather_fstar(const double* __restrict__ F, con
     return tp.ghost[gface][k];
   }
   return F[src * n + k];
+}
+
+// Copy the shift table into shared memory (call with all threads, then __syncthreads()).
+__device__ __forceinline__ void load_delta(const TransportParams& tp, int8_t (*sdelta)[kMaxN]) {
+  for (int i = threadIdx.x; i < 3 * kMaxN; i += blockDim.x) sdelta[i / kMaxN][i % kMaxN] = tp.delta[i / kMaxN][i % kMaxN];
 }
 
 __device__ __forceinline__ double node_v(int k, double L, double dv) { return -L + (k + 0.5) * dv; }

@@ -20,7 +20,7 @@ struct Cfg2 {
   static constexpr int GROUPS = N == 32 ? 6 : 8;   // cells per CTA
   static constexpr int THREADS = GROUPS * N;
   static constexpr size_t PER_GROUP = (size_t)N * N * 16 + (size_t)N * RS * 16;
-  static constexpr size_t SMEM = GROUPS * PER_GROUP;
+  static constexpr size_t SMEM = GROUPS * PER_GROUP + 3 * kMaxN;  // + int8 shift table
 };
 
 template <int N>
@@ -43,15 +43,19 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
   const unsigned lane = threadIdx.x & 31;
   const unsigned mask = N >= 32 ? 0xffffffffu : (((1u << N) - 1u) << (lane & ~(unsigned)(N - 1)));
   const int ngroups = gridDim.x * C::GROUPS;
+  int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::GROUPS * C::PER_GROUP);
+  load_delta(p.tp, sdelta);
+  __syncthreads();
 
   for (int it = blockIdx.x * C::GROUPS + g; it < p.ncells; it += ngroups) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    const CellCoord cc = cell_coord(p.tp, cell);
     // a3: row y = tx of f*, forward FFT along x
     {
       double2 r[N];
 #pragma unroll
       for (int x = 0; x < N; ++x)
-        r[x] = make_double2(gather_fstar(p.f_in, p.tp, cell, x + N * tx, x, tx, 0, n), 0.0);
+        r[x] = make_double2(gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta), 0.0);
       fft<N, -1>(r);
 #pragma unroll
       for (int x = 0; x < N; ++x) wk[tx * RS + x] = r[x];
@@ -95,7 +99,7 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
         } else {
 #pragma unroll
           for (int x = 0; x < N; ++x) {
-            const double fs = gather_fstar(p.f_in, p.tp, cell, x + N * tx, x, tx, 0, n);
+            const double fs = gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta);
             gacc[x] = gacc[x] - fs * r[x].x;  // gacc now holds Q
           }
         }
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
     for (int x = 0; x < N; ++x) {
       const double vx = node_v(x, p.L, p.dv);
       const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * (vx * vx + vy * vy);
-      const double fs = gather_fstar(p.f_in, p.tp, cell, x + N * tx, x, tx, 0, n);
+      const double fs = gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta);
       const double o = fma(p.dt_tau, q[x] - corr, fs);
       bad |= !isfinite(o);
       out[x + N * tx] = o;

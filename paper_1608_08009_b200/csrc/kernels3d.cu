@@ -65,7 +65,8 @@ struct Cfg3 {
   static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;  // tbar, wbar[2]
   static constexpr size_t OFF_TMEM = OFF_MBAR + 24;
   static constexpr size_t OFF_PART = OFF_TMEM + 8;
-  static constexpr size_t SMEM = OFF_PART + 8 * 8;
+  static constexpr size_t OFF_DELTA = OFF_PART + 8 * 8;  // int8 [3][kMaxN] shift table
+  static constexpr size_t SMEM = OFF_DELTA + 3 * kMaxN;
   static_assert(GT % 32 == 0, "warp groups must be whole warps");
   static_assert(GT <= 128, "one TMEM lane per z-group thread");
   static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM allocation: power of two >= 32");
@@ -174,6 +175,7 @@ struct Ctx3 {
   uint64_t* tbar;  // table slab landed
   uint64_t* wbar;  // [2] plane slab landed
   double* part;    // [5] this CTA's moment partial sums (read through DSMEM)
+  const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
   double2* W;      // [NBUF][N j_z][N l_y][RS l_x] exchange buffers of this cluster (L2)
   int rank, cid, ncl, tg, tx, tl;
 };
@@ -311,6 +313,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
   uint32_t wphase = 0;  // bit b = parity of plane buffer b
   for (int it = cid; it < p.ncells; it += c.ncl) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    const CellCoord cc_cell = cell_coord(p.tp, cell);
     const int z = rank * NP + tl;
     // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[2]
     {
@@ -324,7 +327,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         for (int j = 0; j < B; ++j) {
           const int e = tg + (b0 + j) * GT;
           const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
-          v[j] = gather_fstar(p.f_in, p.tp, cell, x + N * (y + N * zz), x, y, zz, n);
+          v[j] = gather_fstar(p.f_in, p.tp, cc_cell, x + N * (y + N * zz), x, y, zz, n, c.delta);
         }
 #pragma unroll
         for (int j = 0; j < B; ++j) {
@@ -391,7 +394,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
           } else {
 #pragma unroll
             for (int y = 0; y < N; ++y) {
-              const double fs = gather_fstar(p.f_in, p.tp, cell, tx + N * (y + N * z), tx, y, z, n);
+              const double fs = gather_fstar(p.f_in, p.tp, cc_cell, tx + N * (y + N * z), tx, y, z, n, c.delta);
               q[y] = q[y] - fs * cc[y].x;  // Q = G - f* c
             }
           }
@@ -438,7 +441,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         const double vy = node_v(y, p.L, p.dv);
         const int k = tx + N * (y + N * z);
         const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * vz + lam[4] * (vx * vx + vy * vy + vz * vz);
-        const double fs = gather_fstar(p.f_in, p.tp, cell, k, tx, y, z, n);
+        const double fs = gather_fstar(p.f_in, p.tp, cc_cell, k, tx, y, z, n, c.delta);
         const double o = fma(p.dt_tau, q[y] - corr, fs);
         bad |= !isfinite(o);
         out[k] = o;
@@ -466,6 +469,9 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.tbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
   c.wbar = c.tbar + 1;
   c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
+  int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::OFF_DELTA);
+  load_delta(p.tp, sdelta);
+  c.delta = sdelta;
   c.rank = (int)cluster.block_rank();
   c.cid = blockIdx.x / P;
   c.ncl = gridDim.x / P;

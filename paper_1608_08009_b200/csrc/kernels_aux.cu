@@ -8,11 +8,15 @@ namespace fks {
 // One CTA row per cell slice: grid (chunks, cells); each thread moves 2 consecutive velocities.
 __global__ void k_transport(const double* __restrict__ f_in, double* __restrict__ f_out, const TransportParams tp,
                             const uint8_t* __restrict__ solid, int64_t ncells, int n, int N, int dv) {
+  __shared__ int8_t sdelta[3][kMaxN];
+  load_delta(tp, sdelta);
+  __syncthreads();
   for (int64_t cell = blockIdx.y; cell < ncells; cell += gridDim.y) {
     const bool is_solid = solid != nullptr && solid[cell];
+    const CellCoord cc = cell_coord(tp, cell);
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
       const int kx = k % N, ky = (k / N) % N, kz = dv == 3 ? k / (N * N) : 0;
-      const double v = is_solid ? f_in[cell * n + k] : gather_fstar(f_in, tp, cell, k, kx, ky, kz, n);
+      const double v = is_solid ? f_in[cell * n + k] : gather_fstar(f_in, tp, cc, k, kx, ky, kz, n, sdelta);
       f_out[cell * n + k] = v;
     }
   }
