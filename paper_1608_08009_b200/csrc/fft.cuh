@@ -1,4 +1,4 @@
-// Register-resident radix-2 FFTs of length 8/16/32 in fp64 for sm_100a.
+// Register-resident radix-2^2 FFTs of length 8/16/32 in fp64 for sm_100a.
 //
 // The paper evaluates its A convolutions with "standard FFT technique" (FFTW 3.3.4 in
 // its runs).  Here one thread owns one whole 1D pencil in registers; the compiler
@@ -58,18 +58,41 @@ __device__ __forceinline__ constexpr int bitrev(int j) {
 }
 
 // In-place DFT of length N (power of two, <= 64): x_j <- sum_k x_k exp(SIGN 2 pi i j k / N).
-// Unnormalised in both directions.
+// Unnormalised in both directions.  Radix-2^2 decimation in frequency: two radix-2 stages are
+// fused per block of M points (quarter Q = M/4) so the inner twiddle is the free +-i and only
+// three twiddles W_M^{2k}, W_M^{k}, W_M^{3k} remain (four in plain radix-2); the data flow and
+// hence the bit-reversed output order are those of radix-2 DIF.  A final radix-2 stage handles
+// odd log2 N.
 template <int N, int SIGN>
 __device__ __forceinline__ void fft(double2 (&x)[N]) {
 #pragma unroll
-  for (int half = N / 2; half >= 1; half >>= 1) {
+  for (int M = N; M >= 4; M >>= 2) {
+    const int Q = M / 4;
 #pragma unroll
-    for (int start = 0; start < N; start += 2 * half) {
+    for (int start = 0; start < N; start += M) {
 #pragma unroll
-      for (int k = 0; k < half; ++k) {
-        const double2 a = x[start + k], b = x[start + k + half];
-        x[start + k] = make_double2(a.x + b.x, a.y + b.y);
-        x[start + k + half] = twiddle<SIGN>(make_double2(a.x - b.x, a.y - b.y), k * (64 / (2 * half)));
+      for (int k = 0; k < Q; ++k) {
+        const double2 a0 = x[start + k], a1 = x[start + k + Q], a2 = x[start + k + 2 * Q],
+                      a3 = x[start + k + 3 * Q];
+        const double2 u0 = make_double2(a0.x + a2.x, a0.y + a2.y);
+        const double2 u2 = make_double2(a0.x - a2.x, a0.y - a2.y);
+        const double2 u1 = make_double2(a1.x + a3.x, a1.y + a3.y);
+        const double2 d13 = make_double2(a1.x - a3.x, a1.y - a3.y);
+        // u3 = (a1 - a3) * (SIGN i)
+        const double2 u3 = SIGN > 0 ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
+        x[start + k] = make_double2(u0.x + u1.x, u0.y + u1.y);
+        const int step = 64 / M;
+        x[start + k + Q] = twiddle<SIGN>(make_double2(u0.x - u1.x, u0.y - u1.y), 2 * k * step);
+        x[start + k + 2 * Q] = twiddle<SIGN>(make_double2(u2.x + u3.x, u2.y + u3.y), k * step);
+        x[start + k + 3 * Q] = twiddle<SIGN>(make_double2(u2.x - u3.x, u2.y - u3.y), 3 * k * step);
+      }
+    }
+    if (M / 4 == 2) {  // one radix-2 stage left (log2 N odd)
+#pragma unroll
+      for (int start = 0; start < N; start += 2) {
+        const double2 a = x[start], b = x[start + 1];
+        x[start] = make_double2(a.x + b.x, a.y + b.y);
+        x[start + 1] = make_double2(a.x - b.x, a.y - b.y);
       }
     }
   }

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -439,6 +441,7 @@ fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double k
   }
   if (st == FKS_OK && dv == 3) {
     c->nclusters = fks::max_active_clusters3d(Nv);
+    if (getenv("FKS_VERBOSE")) fprintf(stderr, "fks: N=%d, %d resident clusters\n", Nv, c->nclusters);
     if (c->nclusters <= 0) st = FKS_E_CUDA;
     else if (cudaMalloc(&c->d_scratch, (size_t)c->nclusters * fks::scratch_elems3d(Nv) * sizeof(double2)) != cudaSuccess)
       st = FKS_E_NOMEM;

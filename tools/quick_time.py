@@ -28,3 +28,4 @@ def run(name, ncells=None, steps=5):
 
 run("C1", steps=10)
 run("C2", steps=3)
+from paper_1608_08009_b200 import _lib
