@@ -53,10 +53,11 @@ struct Cfg3 {
   static constexpr int NP = N / P;        // planes per CTA
   static constexpr int GT = N * NP;       // threads per warp group (one pencil / row / column each)
   static constexpr int THREADS = 2 * GT;  // z group + xy group (warp-specialised)
-  static constexpr int RS = N + 1;        // padded row stride (bank-conflict-free rows and columns)
+  // Planes (SMEM and the L2 exchange buffer) are XOR-swizzled instead of padded: element
+  // (row r, column c) lives at r*N + (c ^ (r & 7)), conflict-free for row and column sweeps.
   static constexpr int SLAB = NP * N * N;     // complex elements of the f^ / table slab
-  static constexpr int PSLAB = NP * N * RS;   // complex elements of a padded plane slab
-  static constexpr int WPLANE = N * RS;       // padded plane in the exchange buffer
+  static constexpr int PSLAB = NP * N * N;    // complex elements of a plane slab
+  static constexpr int WPLANE = N * N;        // plane in the exchange buffer
   static constexpr size_t WBUF = (size_t)N * WPLANE;  // one exchange buffer (all N j_z planes)
   static constexpr int NBUF = 4;  // z stores z(k+1) while phase k is still completing
   static constexpr int TMEM_COLS = 4 * N;     // one f^ pencil (N complex fp64) per lane
@@ -154,6 +155,8 @@ __device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbu
   fft<N, +1>(x);
 }
 
+__device__ __forceinline__ int swz(int r, int c) { return c ^ (r & 7); }
+
 // z-pass output -> this CTA's rows of the exchange buffer (L2): 32 coalesced 512-byte warp stores.
 // L2 write bandwidth (~7.8 TB/s chip-wide, tools/microbench/mb_store.cu) bounds the exchange;
 // staging through SMEM + bulk (TMA) stores was measured slower: the TMA engine reads the staging
@@ -161,7 +164,8 @@ __device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbu
 template <int N, int P>
 __device__ __forceinline__ void zpass_store(const double2 (&x)[N], double2* Wb, int rank, int tx, int tl) {
   using C = Cfg3<N, P>;
-  double2* w = Wb + (size_t)(rank * C::NP + tl) * C::RS + tx;
+  const int ly = rank * C::NP + tl;
+  double2* w = Wb + (size_t)ly * N + swz(ly, tx);
 #pragma unroll
   for (int jz = 0; jz < N; ++jz) w[(size_t)jz * C::WPLANE] = x[jz];
 }
@@ -171,12 +175,12 @@ template <int N, int P>
 struct Ctx3 {
   using C = Cfg3<N, P>;
   double2* tbuf;   // [NP l_y][N l_z][N l_x] table slab of the current direction
-  double2* pln0;   // 2 x [NP j_z][N y][RS x] plane slabs
+  double2* pln0;   // 2 x [NP j_z][N y][N x] plane slabs (swizzled)
   uint64_t* tbar;  // table slab landed
   uint64_t* wbar;  // [2] plane slab landed
   double* part;    // [5] this CTA's moment partial sums (read through DSMEM)
   const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
-  double2* W;      // [NBUF][N j_z][N l_y][RS l_x] exchange buffers of this cluster (L2)
+  double2* W;      // [NBUF][N j_z][N l_y][N l_x] exchange buffers of this cluster (L2, swizzled)
   int rank, cid, ncl, tg, tx, tl;
 };
 
@@ -226,7 +230,7 @@ __device__ __forceinline__ void project_lambda(const StepParams& p, const Ctx3<N
 template <int N, int P>
 __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c, uint32_t taddr) {
   using C = Cfg3<N, P>;
-  constexpr int NP = C::NP, RS = C::RS, GT = C::GT;
+  constexpr int NP = C::NP, GT = C::GT;
   constexpr int n = N * N * N;
   constexpr uint32_t kTabBytes = C::SLAB * 16;
   const int D = p.A + 1;
@@ -237,7 +241,8 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
     cluster_sync_all();  // forward xy-FFT of every CTA stored in W[2]
     {
       double2 x[N];
-      const double2* Wb = c.W + 2 * C::WBUF + (size_t)(rank * NP + tl) * RS + tx;
+      const int ly = rank * NP + tl;
+      const double2* Wb = c.W + 2 * C::WBUF + (size_t)ly * N + swz(ly, tx);
 #pragma unroll
       for (int zz = 0; zz < N; ++zz) x[zz] = __ldcg(Wb + (size_t)zz * C::WPLANE);
       fft<N, -1>(x);
@@ -305,7 +310,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
 template <int N, int P>
 __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& c) {
   using C = Cfg3<N, P>;
-  constexpr int NP = C::NP, RS = C::RS, GT = C::GT;
+  constexpr int NP = C::NP, GT = C::GT;
   constexpr int n = N * N * N;
   constexpr uint32_t kPlaneBytes = C::PSLAB * 16;
   const int D = p.A + 1;
@@ -333,30 +338,30 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         for (int j = 0; j < B; ++j) {
           const int e = tg + (b0 + j) * GT;
           const int x = e % N, y = (e / N) % N, zl = e / (N * N);
-          pln[zl * N * RS + y * RS + x] = make_double2(v[j], 0.0);
+          pln[zl * N * N + y * N + swz(y, x)] = make_double2(v[j], 0.0);
         }
       }
       named_bar(2, GT);
       {
         double2 r[N];
-        double2* row = pln + tl * N * RS + tx * RS;  // row y = tx of plane tl
+        double2* row = pln + tl * N * N + tx * N;  // row y = tx of plane tl
 #pragma unroll
-        for (int x = 0; x < N; ++x) r[x] = row[x];
+        for (int x = 0; x < N; ++x) r[x] = row[swz(tx, x)];
         fft<N, -1>(r);
 #pragma unroll
-        for (int x = 0; x < N; ++x) row[x] = r[x];
+        for (int x = 0; x < N; ++x) row[swz(tx, x)] = r[x];
       }
       named_bar(2, GT);
       {
         double2 cc[N];
-        const double2* col = pln + tl * N * RS + tx;  // column l_x = tx of plane tl
+        const double2* col = pln + tl * N * N;  // column l_x = tx of plane tl
 #pragma unroll
-        for (int y = 0; y < N; ++y) cc[y] = col[y * RS];
+        for (int y = 0; y < N; ++y) cc[y] = col[y * N + swz(y, tx)];
         named_bar(2, GT);  // pln free
         fft<N, -1>(cc);
-        double2* Wb = c.W + 2 * C::WBUF + (size_t)z * C::WPLANE + tx;
+        double2* Wb = c.W + 2 * C::WBUF + (size_t)z * C::WPLANE;
 #pragma unroll
-        for (int ly = 0; ly < N; ++ly) Wb[ly * RS] = cc[ly];
+        for (int ly = 0; ly < N; ++ly) Wb[ly * N + swz(ly, tx)] = cc[ly];
       }
     }
     cluster_sync_all();
@@ -376,16 +381,16 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         // passes keeps the hot loop's instruction footprint small.
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
-          double2* vec = pass == 0 ? pln + tl * N * RS + tx * RS : pln + tl * N * RS + tx;
-          const int stride = pass == 0 ? 1 : RS;
+          double2* pl = pln + tl * N * N;  // pass 0: row y = tx; pass 1: column x = tx
+          auto at = [&](int i) { return pass == 0 ? tx * N + swz(tx, i) : i * N + swz(i, tx); };
           double2 cc[N];
 #pragma unroll
-          for (int x = 0; x < N; ++x) cc[x] = vec[x * stride];
+          for (int x = 0; x < N; ++x) cc[x] = pl[at(x)];
           if (pass == 1) named_bar(2, GT);  // plane buffer pb free for the bulk copy of W(k)
           fft<N, +1>(cc);
           if (pass == 0) {
 #pragma unroll
-            for (int x = 0; x < N; ++x) vec[x] = cc[x];
+            for (int x = 0; x < N; ++x) pl[at(x)] = cc[x];
             named_bar(2, GT);
             TSTAMP(k * 8 + 2);
           } else if (d < p.A) {
@@ -582,7 +587,7 @@ int max_active_clusters3d(int N) {
   }
 }
 
-size_t scratch_elems3d(int N) { return (size_t)Cfg3<32, 8>::NBUF * N * N * (N + 1); }
+size_t scratch_elems3d(int N) { return (size_t)Cfg3<32, 8>::NBUF * N * N * N; }
 
 #ifdef FKS_TIMING
 extern "C" int fks_debug_tstamps(long long* out, int count) {
