@@ -63,10 +63,14 @@ __device__ __forceinline__ constexpr int bitrev(int j) {
 // three twiddles W_M^{2k}, W_M^{k}, W_M^{3k} remain (four in plain radix-2); the data flow and
 // hence the bit-reversed output order are those of radix-2 DIF.  A final radix-2 stage handles
 // odd log2 N.
-template <int N, int SIGN>
-__device__ __forceinline__ void fft(double2 (&x)[N]) {
+// hook(h) is called before each radix-4 stage, before the final radix-2 stage (if any) and after
+// the last stage (h = 0, 1, ...): callers interleave independent memory work with the butterflies.
+template <int N, int SIGN, typename Hook>
+__device__ __forceinline__ void fft_hooked(double2 (&x)[N], Hook&& hook) {
+  int h = 0;
 #pragma unroll
   for (int M = N; M >= 4; M >>= 2) {
+    hook(h++);
     const int Q = M / 4;
 #pragma unroll
     for (int start = 0; start < N; start += M) {
@@ -88,6 +92,7 @@ __device__ __forceinline__ void fft(double2 (&x)[N]) {
       }
     }
     if (M / 4 == 2) {  // one radix-2 stage left (log2 N odd)
+      hook(h++);
 #pragma unroll
       for (int start = 0; start < N; start += 2) {
         const double2 a = x[start], b = x[start + 1];
@@ -96,11 +101,17 @@ __device__ __forceinline__ void fft(double2 (&x)[N]) {
       }
     }
   }
+  hook(h++);
   double2 y[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) y[j] = x[bitrev<N>(j)];
 #pragma unroll
   for (int j = 0; j < N; ++j) x[j] = y[j];
+}
+
+template <int N, int SIGN>
+__device__ __forceinline__ void fft(double2 (&x)[N]) {
+  fft_hooked<N, SIGN>(x, [](int) {});
 }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
