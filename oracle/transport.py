@@ -37,22 +37,23 @@ def shift_delta(n, N, L, dt, dx):
     return shift_s(n + 1, N, L, dt, dx) - shift_s(n, N, L, dt, dx)
 
 
-def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None):
+def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None, cells=None):
     """f* from F^n.  bc: list of 2*dxdim face kinds [lo0, hi0, lo1, hi1, ...].
-    ghosts: dict face -> ghost vector of shape (N,)*dv."""
+    ghosts: dict face -> ghost vector of shape (N,)*dv.  cells: optional flat cell indices; then
+    only those cells are computed and returned as [len(cells), (N,)*dv]."""
     if dxdim == 0:
-        return F.copy()
+        return F.copy() if cells is None else F.reshape((-1,) + F.shape[dxdim:])[list(cells)].copy()
     sp_shape = F.shape[:dxdim]          # (M_{dx-1}, ..., M_0)
     M = sp_shape[::-1]                  # M[a] = cells along space axis a
     delta = shift_delta(n, N, L, dt, dx)
     vshape = (N,) * dv
-    out = np.empty_like(F)
+    out = np.empty_like(F) if cells is None else None
     # velocity-axis index array per component a: component a is array axis dv-1-a
     kcomp = np.meshgrid(*([np.arange(N)] * dv), indexing="ij")
     kcomp = [kcomp[dv - 1 - a] for a in range(dv)]
-    jgrid = np.meshgrid(*[np.arange(m) for m in sp_shape], indexing="ij")
-    jgrid = [jgrid[dxdim - 1 - a] for a in range(dxdim)]  # jgrid[a]: index along space axis a
-    for jflat in range(int(np.prod(sp_shape))):
+    todo = range(int(np.prod(sp_shape))) if cells is None else list(cells)
+    sub = None if cells is None else np.empty((len(todo),) + vshape)
+    for pos, jflat in enumerate(todo):
         jidx = np.unravel_index(jflat, sp_shape)
         j = [jidx[dxdim - 1 - a] for a in range(dxdim)]
         src = []
@@ -78,5 +79,8 @@ def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None):
         if ghosts is not None:
             for face, gv in ghosts.items():
                 vals = np.where(ghost_face == face, gv, vals)
-        out[jidx] = vals
-    return out
+        if sub is None:
+            out[jidx] = vals
+        else:
+            sub[pos] = vals
+    return out if sub is None else sub

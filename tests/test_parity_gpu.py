@@ -323,3 +323,41 @@ def test_slab_partition_bitwise(torch, fks, dxd, dv, M, N, bc, world):
             c.step(loc, o, dt)
             assert torch.equal(o, parallel.local_slice(s, out)), (step, s.rank)
         G = out
+
+
+@pytest.mark.parametrize("name,sample", [("C3", [0, 1, 199, 200, 398, 399]),
+                                         ("C4", [0, 99, 4236, 4237, 5050, 9999])])
+def test_full_size_spatial_sampled(torch, fks, name, sample):
+    """BASELINE configs C3 (1Dx3D Sod, 400 cells, Dirichlet ghosts) and C4 (2Dx3D, 100^2 cells,
+    inflow/outflow, solid boxes) at full size in bench.py's launch configuration: one fused step,
+    sampled cells (faces, interior, next to the solids) against the oracle cell by cell."""
+    from oracle import projection as oproj
+    c = workloads.config(name)
+    N, L, A, dv, dxd = c["N"], c["L"], c["A"], c["dv"], c["dx_dim"]
+    M = list(c["cells"][::-1])
+    F = workloads.initial_state(c)
+    if name == "C4":  # break the uniformity so the transport is visible
+        F = F * (1.0 + 0.1 * np.random.default_rng(9).random(F.shape[:dxd]))[(...,) + (None,) * dv]
+    ghosts = workloads.ghost_vectors(c)
+    solid = workloads.solid_mask(c)
+    ctx = fks.Context(dv, dxd, M, N, L, A, h=c["dx"], bc=c["bc"])
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    if solid is not None:
+        ctx.set_solid(solid)
+    ctx.set_params(tau=c["tau"])
+    fin = dev(torch, F)
+    out = torch.empty_like(fin)
+    ctx.step(fin, out, c["dt"])
+    ctx.check()
+    got = host(out).reshape((-1,) + (N,) * dv)
+    tab = tables.build_tables(dv, N, L)
+    fstar = transport.gather(F, 0, dxd, dv, N, L, c["dt"], c["dx"], c["bc"], ghosts, cells=sample)
+    flatF = F.reshape((-1,) + (N,) * dv)
+    for i, cell in enumerate(sample):
+        if solid is not None and solid.reshape(-1)[cell]:
+            np.testing.assert_array_equal(got[cell], flatF[cell])
+            continue
+        Q = oproj.project_zero_moments(collision.collide_fft(fstar[i], tab), dv, N, L)
+        ref = fstar[i] + (c["dt"] / c["tau"]) * Q
+        assert np.max(np.abs(got[cell] - ref)) <= TOL * np.max(np.abs(ref)), (name, cell)
