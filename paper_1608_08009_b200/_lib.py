@@ -4,7 +4,9 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfks.so")
+# FKS_LIB_VARIANT=<tag> loads libfks_<tag>.so (an in-tree development build of a kernel variant).
+_VARIANT = os.environ.get("FKS_LIB_VARIANT")
+LIB_PATH = os.path.join(HERE, f"libfks_{_VARIANT}.so" if _VARIANT else "libfks.so")
 
 c_int, c_int64, c_double, c_void_p = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 P_DOUBLE = ctypes.POINTER(ctypes.c_double)

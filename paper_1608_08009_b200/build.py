@@ -9,7 +9,7 @@ LIB = os.path.join(HERE, "libfks.so")
 SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels3d.cu", "kernels_aux.cu"]
 HEADERS = ["fft.cuh", "common.cuh", "kernels.cuh", os.path.join("..", "..", "include", "fks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + os.environ.get("FKS_NVCC_EXTRA", "").split() + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v",
          "--expt-relaxed-constexpr"]
 

@@ -42,12 +42,13 @@ int main() {
   double2* buf; CK(cudaMalloc(&buf, (size_t)SM * 65536 * 64));
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b); float ms;
   const int iters = 2000;
-  for (int ns : {1, 4, 8, 64}) for (int th : {128, 512}) {
-    k_stg<<<SM, th>>>(buf, 10, ns);
-    cudaEventRecord(a); k_stg<<<SM, th>>>(buf, iters, ns); cudaEventRecord(b); CK(cudaEventSynchronize(b));
+  for (int nsm : {1, 8, 16, 74, 148}) for (int th : {128, 256}) {
+    const int ns = 8;
+    k_stg<<<nsm, th>>>(buf, 10, ns);
+    cudaEventRecord(a); k_stg<<<nsm, th>>>(buf, iters, ns); cudaEventRecord(b); CK(cudaEventSynchronize(b));
     cudaEventElapsedTime(&ms, a, b);
-    double bytes = 65536.0 * iters * SM;
-    printf("STG.128 %4d threads, %2d slices (%.1f MB): %.1f GB/s total, %.1f B/clk/SM\n", th, ns, ns * SM * 65536 / 1e6, bytes / ms / 1e6, bytes / (ms * 1e-3) / SM / (clk * 1e3));
+    double bytes = 65536.0 * iters * nsm;
+    printf("STG.128 %3d SMs %4d threads: %.1f GB/s total, %.1f B/clk/SM\n", nsm, th, bytes / ms / 1e6, bytes / (ms * 1e-3) / nsm / (clk * 1e3));
   }
   CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   k_bulk<<<SM, 128, 65536>>>(buf, 10);

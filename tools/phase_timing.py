@@ -18,8 +18,20 @@ _lib.load().fks_debug_tstamps(buf, 4096)
 ts = np.array(buf[:])
 base = ts[2 * 8]
 def r(v): return v - base if v else -1
-print("k | xy: top  Wland  xdone  ydone  arrive  waitret  issued | z: arrive Tland zcomp waitret stored")
+print("k | xy: top  Wland  xdone  ydone  arrive  waitret  issued | z: top acq released stored waitret computed barred")
 for k in range(27):
     xy = [r(v) for v in ts[k*8:k*8+7]]
-    z = [r(v) for v in ts[2048+k*8:2048+k*8+5]]
+    z = [r(v) for v in ts[2048+k*8:2048+k*8+7]]
     print(k, "|", " ".join(f"{v:7d}" for v in xy), "|", " ".join(f"{v:7d}" for v in z))
+if ts[1024]:
+    print("chunk consume: t0 | wait  lds+st  bar  issue (cycles)")
+    for g in range(64):
+        v = ts[1024 + g * 8:1024 + g * 8 + 5]
+        if v[0]:
+            print(g, v[0] - base, "|", " ".join(f"{v[i+1]-v[i]:6d}" for i in range(4)))
+if ts[3072 + 8]:
+    print("table slab g (cp_thr: wait-tbar start, landed, cp issued | ld_thr: wait-tcp start, cp done)")
+    for g in range(1, 40):
+        v = ts[3072 + g * 8:3072 + g * 8 + 8]
+        if v[0] or v[3]:
+            print(g, " ".join(f"{(x - base) if x else -1:7d}" for x in v))
