@@ -30,8 +30,14 @@ struct Cfg2 {
   static constexpr size_t OFF_DELTA = GROUPS * PER_GROUP;
   static constexpr size_t OFF_TMEM = OFF_DELTA + 3 * kMaxN + 8;  // 8-byte aligned slot
   static constexpr size_t OFF_TAB = (OFF_TMEM + 4 + 127) / 128 * 128;
-  static constexpr int FCOLS = 4 * N;                          // TMEM columns per thread
-  static constexpr int TMEM_COLS = (THREADS / 128) * FCOLS;    // threads per lane x FCOLS
+  static constexpr int FCOLS = 4 * N;                          // TMEM columns per thread: f^ column
+  // f* row cache (N >= 16): row j_y = tx of f* (N fp64 = 2N columns), read back by the loss
+  // term and the Euler update instead of re-gathering f from global memory.
+  static constexpr bool FS_TMEM = N >= 16;
+  static constexpr int SCOLS = FS_TMEM ? 2 * N : 0;
+  static constexpr int USED_COLS = (THREADS / 128) * (FCOLS + SCOLS);
+  static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
+                                 : USED_COLS <= 256 ? 256 : 512;
   static size_t smem(int A, bool tab_smem) {
     return OFF_TAB + (tab_smem ? (size_t)(A + 1) * N * HC * 16 : 0);
   }
@@ -113,6 +119,17 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
   const uint32_t tbase = *tmem_slot;
   const int w = threadIdx.x >> 5;
   const uint32_t taddr = tbase + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * C::FCOLS);
+  // f* row cache of this thread (FS_TMEM)
+  const uint32_t saddr = tbase + ((uint32_t)(32 * (w & 3)) << 16) +
+                         (uint32_t)((C::THREADS / 128) * C::FCOLS + (w >> 2) * C::SCOLS);
+  // f*(x, j_y = tx) for x in [16 ch, 16 ch + 16): from the TMEM row cache
+  auto fs_chunk = [&](int ch, double (&fs)[16]) {
+    uint32_t v[32];
+    tmem2_ld32(saddr + ch * 32, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) fs[i] = __hiloint2double(v[2 * i + 1], v[2 * i]);
+  };
 
   for (int base = blockIdx.x * C::GROUPS + (threadIdx.x >> 5) * CPW; base < p.ncells; base += stride) {
     const int itr = base + ((threadIdx.x & 31) / N) % CPW;
@@ -120,12 +137,32 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
     const int it = active ? itr : p.ncells - 1;
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
     const CellCoord cc = cell_coord(p.tp, cell);
+    // the next cell of this group (homogeneous case: a contiguous 8 KB row block) -> L2
+    if (p.tp.dx == 0 && tx == 0 && !p.cell_list) {
+      const int nx = itr + stride;
+      if (nx < p.ncells)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.f_in + (int64_t)nx * n),
+                     "r"((uint32_t)(n * sizeof(double)))
+                     : "memory");
+    }
     // a3: row y = tx of f*, forward FFT along x
     {
       double2 r[N];
 #pragma unroll
       for (int x = 0; x < N; ++x)
         r[x] = make_double2(gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta), 0.0);
+      if constexpr (C::FS_TMEM) {
+#pragma unroll
+        for (int ch = 0; ch < N / 16; ++ch) {
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v[2 * i] = __double2loint(r[ch * 16 + i].x);
+            v[2 * i + 1] = __double2hiint(r[ch * 16 + i].x);
+          }
+          tmem2_st32(saddr + ch * 32, v);
+        }
+      }
       fft<N, -1>(r);
 #pragma unroll
       for (int x = 0; x < N; ++x) wk[tx * N + swz2(tx, x)] = r[x];
@@ -193,6 +230,14 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
         if (d < p.A) {
 #pragma unroll
           for (int x = 0; x < N; ++x) gacc[x] = fma(r[x].x, r[x].y, gacc[x]);
+        } else if constexpr (C::FS_TMEM) {
+#pragma unroll
+          for (int ch = 0; ch < N / 16; ++ch) {
+            double fs[16];
+            fs_chunk(ch, fs);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) gacc[ch * 16 + i] = gacc[ch * 16 + i] - fs[i] * r[ch * 16 + i].x;
+          }  // gacc now holds Q
         } else {
 #pragma unroll
           for (int x = 0; x < N; ++x) {
@@ -235,14 +280,24 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
       }
     }
     bool bad = false;
-#pragma unroll
-    for (int x = 0; x < N; ++x) {
+    auto euler = [&](int x, double fs) {
       const double vx = node_v(x, p.L, p.dv);
       const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * (vx * vx + vy * vy);
-      const double fs = gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta);
       const double o = fma(p.dt_tau, q[x] - corr, fs);
       bad |= !isfinite(o);
       if (active) out[x + N * tx] = o;
+    };
+    if constexpr (C::FS_TMEM) {
+#pragma unroll
+      for (int ch = 0; ch < N / 16; ++ch) {
+        double fs[16];
+        fs_chunk(ch, fs);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) euler(ch * 16 + i, fs[i]);
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < N; ++x) euler(x, gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta));
     }
     if (bad && active) atomicOr(p.nonfinite, 1);
   }
