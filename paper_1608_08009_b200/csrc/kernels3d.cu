@@ -60,7 +60,13 @@ struct Cfg3 {
   static constexpr int WPLANE = N * N;        // plane in the exchange buffer
   static constexpr size_t WBUF = (size_t)N * WPLANE;  // one exchange buffer (all N j_z planes)
   static constexpr int NBUF = 4;  // z stores z(k+1) while phase k is still completing
-  static constexpr int TMEM_COLS = 4 * N;     // one f^ pencil (N complex fp64) per lane
+  static constexpr int FHAT_COLS = 4 * N;     // one f^ pencil (N complex fp64) per lane (z group)
+  // f* column cache (xy group, N >= 16): column (l_x = tx, j_z) of f* (N fp64 = 2N columns),
+  // read back by the loss term and the Euler update instead of re-gathering f from HBM.
+  static constexpr bool FS_TMEM = N >= 16;
+  static constexpr int USED_COLS = FHAT_COLS + (FS_TMEM ? 2 * N : 0);
+  static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
+                                 : USED_COLS <= 256 ? 256 : 512;
   static constexpr size_t OFF_TBUF = 0;
   static constexpr size_t OFF_PLN = OFF_TBUF + (size_t)SLAB * 16;  // two plane slabs
   static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;  // tbar, wbar[2]
@@ -308,7 +314,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
 
 // ---- xy group: forward x/y FFT, then xy(k-2) and the gain accumulation, epilogue ------------
 template <int N, int P>
-__device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& c) {
+__device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& c, uint32_t taddr) {
   using C = Cfg3<N, P>;
   constexpr int NP = C::NP, GT = C::GT;
   constexpr int n = N * N * N;
@@ -316,10 +322,25 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
   const int D = p.A + 1;
   const int rank = c.rank, cid = c.cid, tg = c.tg, tx = c.tx, tl = c.tl;
   uint32_t wphase = 0;  // bit b = parity of plane buffer b
+  const uint32_t saddr = taddr + C::FHAT_COLS;  // f* column cache (FS_TMEM)
+  // f*(tx, y, z) for y in [16 ch, 16 ch + 16) from the column cache
+  auto fs_chunk = [&](int ch, double (&fs)[16]) {
+    uint32_t v[32];
+    tmem_ld32(saddr + ch * 32, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) fs[i] = __hiloint2double(v[2 * i + 1], v[2 * i]);
+  };
   for (int it = cid; it < p.ncells; it += c.ncl) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
     const CellCoord cc_cell = cell_coord(p.tp, cell);
     const int z = rank * NP + tl;
+    // this CTA's planes of the next cell (homogeneous case: contiguous) -> L2
+    if (p.tp.dx == 0 && tg == 0 && !p.cell_list && it + c.ncl < p.ncells)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.f_in + (int64_t)(it + c.ncl) * n +
+                                                                        (int64_t)rank * NP * N * N),
+                   "r"((uint32_t)(NP * N * N * sizeof(double)))
+                   : "memory");
     // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[2]
     {
       double2* pln = c.pln0;
@@ -342,6 +363,23 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         }
       }
       named_bar(2, GT);
+      if constexpr (C::FS_TMEM) {  // column (tx, ., tl) of f* -> TMEM cache
+        const double2* col = pln + tl * N * N;
+#pragma unroll
+        for (int ch = 0; ch < N / 16; ++ch) {
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int y = ch * 16 + i;
+            const double f = col[y * N + swz(y, tx)].x;
+            v[2 * i] = __double2loint(f);
+            v[2 * i + 1] = __double2hiint(f);
+          }
+          tmem_st32(saddr + ch * 32, v);
+        }
+        tmem_wait_st();
+        named_bar(2, GT);  // every column read before the rows are transformed in place
+      }
       {
         double2 r[N];
         double2* row = pln + tl * N * N + tx * N;  // row y = tx of plane tl
@@ -396,6 +434,14 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
           } else if (d < p.A) {
 #pragma unroll
             for (int y = 0; y < N; ++y) q[y] = fma(cc[y].x, cc[y].y, q[y]);
+          } else if constexpr (C::FS_TMEM) {
+#pragma unroll
+            for (int ch = 0; ch < N / 16; ++ch) {
+              double fs[16];
+              fs_chunk(ch, fs);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) q[ch * 16 + i] = q[ch * 16 + i] - fs[i] * cc[ch * 16 + i].x;
+            }  // Q = G - f* c
           } else {
 #pragma unroll
             for (int y = 0; y < N; ++y) {
@@ -441,15 +487,26 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         project_lambda<N, P>(p, c, true, m, lam);
       }
       bool bad = false;
-#pragma unroll
-      for (int y = 0; y < N; ++y) {
+      auto euler = [&](int y, double fs) {
         const double vy = node_v(y, p.L, p.dv);
         const int k = tx + N * (y + N * z);
         const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * vz + lam[4] * (vx * vx + vy * vy + vz * vz);
-        const double fs = gather_fstar(p.f_in, p.tp, cc_cell, k, tx, y, z, n, c.delta);
         const double o = fma(p.dt_tau, q[y] - corr, fs);
         bad |= !isfinite(o);
         out[k] = o;
+      };
+      if constexpr (C::FS_TMEM) {
+#pragma unroll
+        for (int ch = 0; ch < N / 16; ++ch) {
+          double fs[16];
+          fs_chunk(ch, fs);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) euler(ch * 16 + i, fs[i]);
+        }
+      } else {
+#pragma unroll
+        for (int y = 0; y < N; ++y)
+          euler(y, gather_fstar(p.f_in, p.tp, cc_cell, tx + N * (y + N * z), tx, y, z, n, c.delta));
       }
       if (bad) atomicOr(p.nonfinite, 1);
       if (p.project) {  // part[] is read remotely before it is rewritten (or the CTA exits);
@@ -507,7 +564,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
     // this thread's TMEM lane: warp quarter base + lane in warp (row field = bits 31..16)
     z_group<N, P>(p, c, tbase + ((uint32_t)(32 * ((t >> 5) & 3)) << 16));
   } else {
-    xy_group<N, P>(p, c);
+    xy_group<N, P>(p, c, tbase + ((uint32_t)(32 * ((t >> 5) & 3)) << 16));
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
