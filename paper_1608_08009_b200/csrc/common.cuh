@@ -22,7 +22,8 @@ struct StepParams {
   const double* f_in;        // F^n       [cells][n]
   double* f_out;             // F^{n+1} or Q [cells][n]
   const double2* tables;     // folded tables, layout per kernel (see kernels*.cu)
-  double2* scratch;          // per-cluster exchange buffers (3D)
+  double2* scratch;          // per-group exchange buffers (3D)
+  unsigned* sync;            // per-group synchronisation counters (3D; zeroed before each launch)
   int* nonfinite;            // device flag
   const int* cell_list;      // fluid cells to process (local linear indices)
   int ncells;                // entries of cell_list

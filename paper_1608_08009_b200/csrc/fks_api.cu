@@ -216,6 +216,7 @@ struct fks_ctx {
   double Ginv[25];
   double2* d_tables = nullptr;
   double2* d_scratch = nullptr;
+  unsigned* d_sync = nullptr;  // 3D group counters
   int* d_flag = nullptr;
   int* d_fluid = nullptr;
   int nfluid = 0;
@@ -238,18 +239,38 @@ fks_status upload_tables(fks_ctx* c) {
   build_tables(c->dv, c->N, c->R, c->dirs, al, alp, D);
   const int n = c->n, N = c->N, A = c->A;
   const double s = node_scale(c->dv, c->L, c->kconst);
-  std::vector<double2> T((size_t)(A + 1) * n);
   // Fold s, w_p and 1/n (the kernels use the unnormalised forward DFT) into the tables.
-  for (int p = 0; p <= A; ++p)
-    for (int k = 0; k < n; ++k) {
-      const int x = k % N, y = (k / N) % N, z = c->dv == 3 ? k / (N * N) : 0;
-      // 3D layout T[p][l_y][l_z][l_x]; 2D layout T[p][l_y][l_x]
-      const size_t dst = c->dv == 3 ? (size_t)p * n + (size_t)y * N * N + (size_t)z * N + x : (size_t)p * n + k;
-      if (p < A)
-        T[dst] = make_double2(s * c->dirs.w[p] * al[(size_t)p * n + k] / n, alp[(size_t)p * n + k] / n);
-      else
-        T[dst] = make_double2(s * D[k] / n, 0.0);
-    }
+  auto folded = [&](int p, int k) {
+    return p < A ? make_double2(s * c->dirs.w[p] * al[(size_t)p * n + k] / n, alp[(size_t)p * n + k] / n)
+                 : make_double2(s * D[k] / n, 0.0);
+  };
+  std::vector<double2> T;
+  if (c->dv == 2) {  // T[p][l_y][l_x]
+    T.resize((size_t)(A + 1) * n);
+    for (int p = 0; p <= A; ++p)
+      for (int k = 0; k < n; ++k) T[(size_t)p * n + k] = folded(p, k);
+  } else {
+    // T3[p][rank][row][l_x]: rank r owns the l_y planes at positions r*NP .. r*NP+NP-1 of the
+    // order 0, N/2, 1, N-1, 2, N-2, ...; it stores the first plane of each mirror pair (N rows
+    // l_z) and the rows l_z <= N/2 of the self-mirror planes 0 and N/2 (kernels3d.cu Cfg3).
+    int P = 0, NP = 0, slabr = 0;
+    if (fks::table_layout3d(N, &P, &NP, &slabr) != 0) return FKS_E_INVAL;
+    auto plane_of = [&](int q) { return q == 0 ? 0 : q == 1 ? N / 2 : (q & 1) ? N - q / 2 : q / 2; };
+    T.assign((size_t)(A + 1) * P * slabr * N, make_double2(0.0, 0.0));
+    for (int p = 0; p <= A; ++p)
+      for (int r = 0; r < P; ++r) {
+        int row = 0;
+        for (int e = 0; e < NP; ++e) {
+          const int ly = plane_of(r * NP + e);
+          int nrows = 0;
+          if (ly == 0 || ly == N / 2) nrows = N / 2 + 1;
+          else if ((e & 1) == 0) nrows = N;
+          for (int lz = 0; lz < nrows; ++lz, ++row)
+            for (int lx = 0; lx < N; ++lx)
+              T[(((size_t)p * P + r) * slabr + row) * N + lx] = folded(p, lx + N * (ly + N * lz));
+        }
+      }
+  }
   if (c->d_tables) cudaFree(c->d_tables);
   c->d_tables = nullptr;
   if (cudaMalloc(&c->d_tables, T.size() * sizeof(double2)) != cudaSuccess) return FKS_E_NOMEM;
@@ -315,6 +336,7 @@ fks::StepParams base_params(fks_ctx* c, const double* f_in, double* f_out, int m
   p.f_out = f_out;
   p.tables = c->d_tables;
   p.scratch = c->d_scratch;
+  p.sync = c->d_sync;
   p.nonfinite = c->d_flag;
   p.A = c->A;
   p.mode = mode;
@@ -331,7 +353,8 @@ fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
   cudaError_t e;
   if (c->dv == 3) {
     const int ncl = std::min<int64_t>(p.ncells, c->nclusters);
-    e = fks::launch_step3d(c->N, p, ncl, c->stream);
+    e = cudaMemsetAsync(c->d_sync, 0, (size_t)ncl * fks::sync_bytes3d(), c->stream);
+    if (e == cudaSuccess) e = fks::launch_step3d(c->N, p, ncl, c->stream);
   } else {
     const int per = fks::cells_per_block2d(c->N);
     const int64_t need = (p.ncells + per - 1) / per;
@@ -441,9 +464,14 @@ fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double k
   }
   if (st == FKS_OK && dv == 3) {
     c->nclusters = fks::max_active_clusters3d(Nv);
-    if (getenv("FKS_VERBOSE")) fprintf(stderr, "fks: N=%d, %d resident clusters\n", Nv, c->nclusters);
+    if (const char* e = getenv("FKS_MAX_CLUSTERS")) {  // development: scaling with the cluster count
+      const int m = atoi(e);
+      if (m > 0 && m < c->nclusters) c->nclusters = m;
+    }
+    if (getenv("FKS_VERBOSE")) fprintf(stderr, "fks: N=%d, %d resident CTA groups\n", Nv, c->nclusters);
     if (c->nclusters <= 0) st = FKS_E_CUDA;
-    else if (cudaMalloc(&c->d_scratch, (size_t)c->nclusters * fks::scratch_elems3d(Nv) * sizeof(double2)) != cudaSuccess)
+    else if (cudaMalloc(&c->d_scratch, (size_t)c->nclusters * fks::scratch_elems3d(Nv) * sizeof(double2)) != cudaSuccess ||
+             cudaMalloc(&c->d_sync, (size_t)c->nclusters * fks::sync_bytes3d()) != cudaSuccess)
       st = FKS_E_NOMEM;
   }
   if (st == FKS_OK) st = set_cell_lists(c, nullptr);
@@ -604,6 +632,7 @@ fks_status fks_finalize(fks_ctx* c) {
   if (!c) return FKS_E_INVAL;
   cudaFree(c->d_tables);
   cudaFree(c->d_scratch);
+  cudaFree(c->d_sync);
   cudaFree(c->d_flag);
   cudaFree(c->d_fluid);
   cudaFree(c->d_solid_list);

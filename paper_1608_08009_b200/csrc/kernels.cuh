@@ -6,10 +6,15 @@
 
 namespace fks {
 
-// 3D (hard spheres): cluster of 8 CTAs per cell; scratch = nclusters * scratch_elems3d(N) double2.
-cudaError_t launch_step3d(int N, const StepParams& p, int nclusters, cudaStream_t s);
-int max_active_clusters3d(int N);
+// 3D (hard spheres): a group of 8 co-resident CTAs per cell (cooperative launch, one CTA per
+// SM); scratch = ngroups * scratch_elems3d(N) double2, sync = ngroups * sync_bytes3d() bytes,
+// zeroed before every launch.
+cudaError_t launch_step3d(int N, const StepParams& p, int ngroups, cudaStream_t s);
+int max_active_clusters3d(int N);  // groups that fit the GPU at once
 size_t scratch_elems3d(int N);
+size_t sync_bytes3d();
+// 3D table layout: P CTAs per cell, NP l_y planes per CTA, slabr rows (of N entries) per CTA slab.
+int table_layout3d(int N, int* P, int* NP, int* slabr);
 
 // 2D (Maxwell molecules): cells_per_block2d(N) cells per CTA.
 cudaError_t launch_step2d(int N, const StepParams& p, int nblocks, cudaStream_t s);

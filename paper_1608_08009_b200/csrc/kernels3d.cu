@@ -28,15 +28,11 @@
 // F^{n+1} = f* + (dt/tau) Pi Q, or Q in collide mode.
 // Tables are pre-folded on the host: alpha~ = s w_p alpha_p / n, alpha'~ = alpha'_p / n,
 // D~ = s D / n (s = Btilde kappa^-(d+gamma)); layout T[p][l_y][l_z][l_x] as double2.
-#include <cooperative_groups.h>
-
 #include <cstdlib>
 
 #include "common.cuh"
 #include "fft.cuh"
 #include "kernels.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace fks {
 
@@ -55,7 +51,13 @@ struct Cfg3 {
   static constexpr int THREADS = 2 * GT;  // z group + xy group (warp-specialised)
   // Planes (SMEM and the L2 exchange buffer) are XOR-swizzled instead of padded: element
   // (row r, column c) lives at r*N + (c ^ (r & 7)), conflict-free for row and column sweeps.
-  static constexpr int SLAB = NP * N * N;     // complex elements of the f^ / table slab
+  // z-side plane ownership pairs every l_y plane with its mirror sigma(l_y) = -l_y mod N: the
+  // planes in the order 0, N/2, 1, N-1, 2, N-2, ... are dealt out NP per CTA.  The tables are
+  // even, T(l) = T(-l) exactly (reading #10), so T(l_x, -a, l_z) = T(-l_x, a, -l_z):
+  // a CTA stores only the first plane of each pair and the rows l_z <= N/2 of the self-mirror
+  // planes 0 and N/2 -- SLABR rows of N complex entries (halves the table traffic).
+  static constexpr int SLABR = (N + 2) + (NP - 2) / 2 * N;  // rows per CTA table slab (rank 0 = max)
+  static constexpr int SLAB = SLABR * N;      // complex elements of a table slab
   static constexpr int PSLAB = NP * N * N;    // complex elements of a plane slab
   static constexpr int WPLANE = N * N;        // plane in the exchange buffer
   static constexpr size_t WBUF = (size_t)N * WPLANE;  // one exchange buffer (all N j_z planes)
@@ -68,13 +70,14 @@ struct Cfg3 {
   static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
                                  : USED_COLS <= 256 ? 256 : 512;
   static constexpr size_t OFF_TBUF = 0;
-  static constexpr size_t OFF_PLN = OFF_TBUF + (size_t)SLAB * 16;  // two plane slabs
+  static constexpr size_t OFF_PLN = OFF_TBUF + ((size_t)SLAB * 16 + 127) / 128 * 128;  // two plane slabs
   static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;  // tbar, wbar[2]
   static constexpr size_t OFF_TMEM = OFF_MBAR + 24;
   static constexpr size_t OFF_PART = OFF_TMEM + 8;
   static constexpr size_t OFF_DELTA = OFF_PART + 8 * 8;  // int8 [3][kMaxN] shift table
   static constexpr size_t SMEM = OFF_DELTA + 3 * kMaxN;
   static_assert(GT % 32 == 0, "warp groups must be whole warps");
+  static_assert(NP % 2 == 0, "mirror pairs stay within a CTA");
   static_assert(GT <= 128, "one TMEM lane per z-group thread");
   static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM allocation: power of two >= 32");
 };
@@ -93,9 +96,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
-__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void cluster_sync_all() { cl_arrive(); cl_wait(); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -139,11 +139,44 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
              bytes - off < chunk ? bytes - off : chunk, bar);
 }
 
+__device__ __forceinline__ int swz(int r, int c) { return c ^ (r & 7); }
+
+// l_y plane at position q of the order 0, N/2, 1, N-1, 2, N-2, ... (z-side plane ownership).
+template <int N>
+__device__ __forceinline__ int plane_of(int q) {
+  return q == 0 ? 0 : q == 1 ? N / 2 : (q & 1) ? N - q / 2 : q / 2;
+}
+
+// Where the z thread of local plane tl finds its table pencil in the CTA's table slab
+// (host layout: fks_api.cu upload_tables): first row and how rows/columns map.
+struct TabMap {
+  int base;  // first slab row of the stored plane
+  int mode;  // 0: stored plane; 1: mirror of the stored plane (row -l_z, column -l_x);
+             // 2: self-mirror plane, rows l_z <= N/2 stored, the others mirrored
+};
+template <int N, int NP>
+__device__ __forceinline__ TabMap tab_map(int rank, int tl) {
+  int base = 0;
+  for (int e = 0; e < tl; ++e) {  // rows taken by the entries before tl
+    const int ly = plane_of<N>(rank * NP + e);
+    if (ly == 0 || ly == N / 2) base += N / 2 + 1;
+    else if ((e & 1) == 0) base += N;
+  }
+  const int ly = plane_of<N>(rank * NP + tl);
+  TabMap m;
+  if (ly == 0 || ly == N / 2) m = {base, 2};
+  else if ((tl & 1) == 0) m = {base, 0};
+  else m = {base - N, 1};  // the pair's first plane, stored just before
+  return m;
+}
+
 // z group: X = T (x) f^ for pencil (l_x = tx, local l_y = tl) of one direction (f^ from this
 // thread's TMEM lane, T from the SMEM table slab), then the IFFT along z, in registers.
 template <int N, int P>
-__device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbuf, int tx, int tl, double2 (&x)[N]) {
-  const double2* tb = tbuf + tl * N * N + tx;
+__device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbuf, int tx, const TabMap& tm,
+                                              double2 (&x)[N]) {
+  const double2* td = tbuf + tm.base * N + tx;             // stored rows, own column
+  const double2* tr = tbuf + tm.base * N + ((N - tx) & (N - 1));  // mirrored column
 #pragma unroll
   for (int ch = 0; ch < N / 8; ++ch) {  // 8 complex fp64 = 32 TMEM columns per chunk
     uint32_t v[32];
@@ -154,26 +187,61 @@ __device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbu
       const int lz = ch * 8 + i;
       const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
       const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
-      const double2 T = tb[lz * N];
+      const int lzm = (N - lz) & (N - 1);
+      const bool mir = tm.mode == 1 || (tm.mode == 2 && lz > N / 2);
+      const double2 T = mir ? tr[lzm * N] : td[lz * N];
       x[lz] = make_double2(fma(T.x, Fx, -T.y * Fy), fma(T.x, Fy, T.y * Fx));
     }
   }
   fft<N, +1>(x);
 }
 
-__device__ __forceinline__ int swz(int r, int c) { return c ^ (r & 7); }
 
 // z-pass output -> this CTA's rows of the exchange buffer (L2): 32 coalesced 512-byte warp stores.
 // L2 write bandwidth (~7.8 TB/s chip-wide, tools/microbench/mb_store.cu) bounds the exchange;
 // staging through SMEM + bulk (TMA) stores was measured slower: the TMA engine reads the staging
 // buffer only as fast as it drains to L2, so the staging slot is not freed any earlier.
 template <int N, int P>
-__device__ __forceinline__ void zpass_store(const double2 (&x)[N], double2* Wb, int rank, int tx, int tl) {
+__device__ __forceinline__ void zpass_store(const double2 (&x)[N], double2* Wb, int ly, int tx) {
   using C = Cfg3<N, P>;
-  const int ly = rank * C::NP + tl;
   double2* w = Wb + (size_t)ly * N + swz(ly, tx);
 #pragma unroll
   for (int jz = 0; jz < N; ++jz) w[(size_t)jz * C::WPLANE] = x[jz];
+}
+
+// Group synchronisation through L2 (the P CTAs of a cell group are co-resident: cooperative
+// launch, one CTA per SM).  Every exchange buffer use is an item of a per-group sequence
+// (per cell: the forward xy transform, then z(0) .. z(D-1)); item s lives in ring slot s % NBUF.
+// Each of the P producers adds 1 to prod[slot] after writing its part (release), each of the P
+// consumers adds 1 to cons[slot] once its read has completed; a producer of item s first waits
+// for cons[slot] >= P * (s / NBUF), a consumer for prod[slot] >= P * (s / NBUF + 1).  The
+// counters are zeroed before every launch.
+struct GroupSync {
+  static constexpr int NB = 4;  // = Cfg3::NBUF
+  unsigned prod[NB];
+  unsigned cons[NB];
+  unsigned part;                // projection partial sums published (cumulative, P per cell)
+  unsigned pad[32 - 2 * NB - 1];
+  double partial[2][16][5];     // [cell parity][rank][moment]
+};
+
+__device__ __forceinline__ void sync_signal(unsigned* ctr) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* ctr) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+  return v;
+}
+
+// Spin until *ctr >= target.  A group member that never arrives would otherwise hang the GPU:
+// after ~2^24 polls (seconds) the kernel traps and the launch fails loudly.
+__device__ __forceinline__ void sync_wait(const unsigned* ctr, unsigned target) {
+  unsigned spins = 0;
+  while ((int)(ld_acquire(ctr) - target) < 0) {
+    if (++spins == (1u << 24)) __trap();
+  }
 }
 
 // Shared-memory carve-up and per-thread coordinates of the 3D kernel.
@@ -184,71 +252,41 @@ struct Ctx3 {
   double2* pln0;   // 2 x [NP j_z][N y][N x] plane slabs (swizzled)
   uint64_t* tbar;  // table slab landed
   uint64_t* wbar;  // [2] plane slab landed
-  double* part;    // [5] this CTA's moment partial sums (read through DSMEM)
+  double* part;    // [8] epilogue scratch (moment sums, lambda)
   const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
-  double2* W;      // [NBUF][N j_z][N l_y][N l_x] exchange buffers of this cluster (L2, swizzled)
+  double2* W;      // [NBUF][N j_z][N l_y][N l_x] exchange buffers of this group (L2, swizzled)
+  GroupSync* gs;   // this group's counters
   int rank, cid, ncl, tg, tx, tl;
 };
 
-// Epilogue moment reduction (a8): xy group supplies m[5] (zeros from the z group); returns
-// lambda = Ginv * sum over the cluster (fixed order: warps, then ranks).
-template <int N, int P>
-__device__ __forceinline__ void project_lambda(const StepParams& p, const Ctx3<N, P>& c, bool xy, double (&m)[5],
-                                               double (&lam)[5]) {
-  using C = Cfg3<N, P>;
-  constexpr int NW = C::GT / 32;
-  double* wpart = reinterpret_cast<double*>(c.pln0);  // plane buffers idle in the epilogue
-  if (xy) {
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
-    }
-    if ((c.tg & 31) == 0) {
-#pragma unroll
-      for (int k = 0; k < 5; ++k) wpart[(c.tg >> 5) * 5 + k] = m[k];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 5) {
-    double s = 0.0;
-    for (int w = 0; w < NW; ++w) s += wpart[w * 5 + threadIdx.x];
-    c.part[threadIdx.x] = s;
-  }
-  cluster_sync_all();
-  cg::cluster_group cluster = cg::this_cluster();
-  double mu[5] = {0, 0, 0, 0, 0};
-  for (int r = 0; r < P; ++r) {
-    const double* rp = cluster.map_shared_rank(c.part, r);
-#pragma unroll
-    for (int k = 0; k < 5; ++k) mu[k] += rp[k];
-  }
-#pragma unroll
-  for (int a = 0; a < 5; ++a) {
-    double s = 0.0;
-#pragma unroll
-    for (int b = 0; b < 5; ++b) s = fma(p.Ginv[a * 5 + b], mu[b], s);
-    lam[a] = s;
-  }
-}
-
-// ---- z group: forward z-FFT into TMEM, then z(k) for every direction ----------------------
+// ---- z group: forward z-FFT into TMEM, then z(j) for every direction ----------------------
 template <int N, int P>
 __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c, uint32_t taddr) {
   using C = Cfg3<N, P>;
-  constexpr int NP = C::NP, GT = C::GT;
+  constexpr int NP = C::NP, GT = C::GT, NB = C::NBUF;
   constexpr int n = N * N * N;
-  constexpr uint32_t kTabBytes = C::SLAB * 16;
   const int D = p.A + 1;
   const int rank = c.rank, cid = c.cid, tg = c.tg, tx = c.tx, tl = c.tl;
+  GroupSync* gs = c.gs;
+  const int ly = plane_of<N>(rank * NP + tl);  // this thread's pencil (l_x = tx, l_y)
+  const TabMap tm = tab_map<N, NP>(rank, tl);
+  // rows of this CTA's table slab (the last entry's extent)
+  const uint32_t kTabBytes = [&] {
+    const TabMap last = tab_map<N, NP>(rank, NP - 1);
+    const int rows = last.mode == 1 ? last.base + N : last.mode == 2 ? last.base + N / 2 + 1 : last.base + N;
+    return (uint32_t)rows * N * 16;
+  }();
+  const double2* tab_rank = p.tables + (size_t)rank * C::SLAB;  // + direction * P * SLAB
   uint32_t tphase = 0;
+  unsigned seq = 0;  // exchange-buffer sequence index of the next item
+  if (tg == 0) bulk_load(c.tbuf, tab_rank, kTabBytes, c.tbar);
   for (int it = cid; it < p.ncells; it += c.ncl) {
-    if (tg == 0) bulk_load(c.tbuf, p.tables + (size_t)rank * C::SLAB, kTabBytes, c.tbar);
-    cluster_sync_all();  // forward xy-FFT of every CTA stored in W[2]
-    {
+    {  // forward item: the xy transforms of every CTA of the group
+      const unsigned slot = seq % NB, use = seq / NB;
+      if (tg == 0) sync_wait(&gs->prod[slot], P * (use + 1));
+      named_bar(1, GT);
       double2 x[N];
-      const int ly = rank * NP + tl;
-      const double2* Wb = c.W + 2 * C::WBUF + (size_t)ly * N + swz(ly, tx);
+      const double2* Wb = c.W + slot * C::WBUF + (size_t)ly * N + swz(ly, tx);
 #pragma unroll
       for (int zz = 0; zz < N; ++zz) x[zz] = __ldcg(Wb + (size_t)zz * C::WPLANE);
       fft<N, -1>(x);
@@ -265,63 +303,53 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
         tmem_st32(taddr + ch * 32, v);
       }
       tmem_wait_st();
+      named_bar(1, GT);  // every column of the forward item read
+      if (tg == 0) sync_signal(&gs->cons[slot]);
+      ++seq;
     }
-    {
+#pragma unroll 1
+    for (int j = 0; j < D; ++j) {
+      TSTAMP(2048 + j * 8);
+      const unsigned slot = seq % NB, use = seq / NB;
       double2 x[N];
       mbar_wait(c.tbar, tphase);
       tphase ^= 1;
-      zpass_compute<N, P>(taddr, c.tbuf, tx, tl, x);
-      named_bar(1, GT);  // tbuf consumed
-      if (tg == 0 && D > 1) bulk_load(c.tbuf, p.tables + (size_t)1 * n + (size_t)rank * C::SLAB, kTabBytes, c.tbar);
-      zpass_store<N, P>(x, c.W, rank, tx, tl);  // z(0) -> W[0]
-    }
-#pragma unroll 1
-    for (int k = 0; k <= D + 1; ++k) {
-      // z(k) was stored before this point; computing z(k+1) first lets the release of
-      // arrive(k) find those stores completed (and overlaps the FFT with the barrier).
-      TSTAMP(2048 + k * 8);
-      double2 x[N];
-      const bool more = k + 1 < D;
-      if (more) {
-        mbar_wait(c.tbar, tphase);
-        tphase ^= 1;
-        TSTAMP(2048 + k * 8 + 1);
-        zpass_compute<N, P>(taddr, c.tbuf, tx, tl, x);
-        named_bar(1, GT);  // tbuf consumed
-        if (tg == 0 && k + 2 < D)
-          bulk_load(c.tbuf, p.tables + (size_t)(k + 2) * n + (size_t)rank * C::SLAB, kTabBytes, c.tbar);
-        TSTAMP(2048 + k * 8 + 2);
+      TSTAMP(2048 + j * 8 + 1);
+      zpass_compute<N, P>(taddr, c.tbuf, tx, tm, x);
+      TSTAMP(2048 + j * 8 + 2);
+      // thread 0: slot free (its previous item read by every consumer) before anyone stores
+      if (tg == 0 && use > 0) sync_wait(&gs->cons[slot], P * use);
+      named_bar(1, GT);  // tbuf consumed; the z(j-1) stores of every thread precede this point
+      if (tg == 0) {
+        // next table slab (wrapping to direction 0 of the next cell)
+        const int dn = j + 1 < D ? j + 1 : 0;
+        if (j + 1 < D || it + c.ncl < p.ncells)
+          bulk_load(c.tbuf, tab_rank + (size_t)dn * P * C::SLAB, kTabBytes, c.tbar);
+        // publish z(j-1): its stores had a whole z pass to drain, so the release is cheap
+        if (j > 0) sync_signal(&gs->prod[(seq - 1) % NB]);
       }
-      cl_arrive();  // phase k: z(k) stored (release; the consumers read it through the async proxy
-                    // after their acquire + fence.proxy.async)
-      // W[(k+1)%4] was last read by xy(k-3), finished everywhere before phase k-1 completed.
-      if (more) zpass_store<N, P>(x, c.W + (size_t)((k + 1) % 4) * C::WBUF, rank, tx, tl);
-      TSTAMP(2048 + k * 8 + 3);
-      cl_wait();    // phase k complete
-      TSTAMP(2048 + k * 8 + 4);
+      zpass_store<N, P>(x, c.W + slot * C::WBUF, ly, tx);
+      TSTAMP(2048 + j * 8 + 3);
+      ++seq;
     }
-    if (p.mode == 1) {
-      if (p.project) {
-        double m[5] = {0, 0, 0, 0, 0}, lam[5];
-        project_lambda<N, P>(p, c, false, m, lam);
-        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
-        cl_wait();
-      }
-    }
-    __syncthreads();
+    named_bar(1, GT);  // the z(D-1) stores of every thread precede the release
+    if (tg == 0) sync_signal(&gs->prod[(seq - 1) % NB]);
   }
 }
 
-// ---- xy group: forward x/y FFT, then xy(k-2) and the gain accumulation, epilogue ------------
+// ---- xy group: forward x/y FFT, then xy(j) and the gain accumulation, epilogue -------------
 template <int N, int P>
 __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& c, uint32_t taddr) {
   using C = Cfg3<N, P>;
-  constexpr int NP = C::NP, GT = C::GT;
+  constexpr int NP = C::NP, GT = C::GT, NB = C::NBUF;
   constexpr int n = N * N * N;
   constexpr uint32_t kPlaneBytes = C::PSLAB * 16;
   const int D = p.A + 1;
   const int rank = c.rank, cid = c.cid, tg = c.tg, tx = c.tx, tl = c.tl;
+  GroupSync* gs = c.gs;
   uint32_t wphase = 0;  // bit b = parity of plane buffer b
+  unsigned seq = 0;     // exchange-buffer sequence index of the next item
+  unsigned ncell = 0;   // cells done by this group
   const uint32_t saddr = taddr + C::FHAT_COLS;  // f* column cache (FS_TMEM)
   // f*(tx, y, z) for y in [16 ch, 16 ch + 16) from the column cache
   auto fs_chunk = [&](int ch, double (&fs)[16]) {
@@ -331,7 +359,13 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
 #pragma unroll
     for (int i = 0; i < 16; ++i) fs[i] = __hiloint2double(v[2 * i + 1], v[2 * i]);
   };
-  for (int it = cid; it < p.ncells; it += c.ncl) {
+  // thread 0: W(item s) -> plane buffer b, once every producer has published it
+  auto issue_load = [&](unsigned s, int b) {
+    sync_wait(&gs->prod[s % NB], P * (s / NB + 1));
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic-proxy stores -> bulk reads
+    bulk_load(c.pln0 + b * C::PSLAB, c.W + (s % NB) * C::WBUF + (size_t)rank * C::PSLAB, kPlaneBytes, c.wbar + b);
+  };
+  for (int it = cid; it < p.ncells; it += c.ncl, ++ncell) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
     const CellCoord cc_cell = cell_coord(p.tp, cell);
     const int z = rank * NP + tl;
@@ -341,7 +375,8 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
                                                                         (int64_t)rank * NP * N * N),
                    "r"((uint32_t)(NP * N * N * sizeof(double)))
                    : "memory");
-    // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[2]
+    const unsigned s_fwd = seq;
+    // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[s_fwd % NB]
     {
       double2* pln = c.pln0;
       constexpr int PER = NP * N * N / GT;  // = N elements per thread
@@ -395,75 +430,70 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         const double2* col = pln + tl * N * N;  // column l_x = tx of plane tl
 #pragma unroll
         for (int y = 0; y < N; ++y) cc[y] = col[y * N + swz(y, tx)];
-        named_bar(2, GT);  // pln free
         fft<N, -1>(cc);
-        double2* Wb = c.W + 2 * C::WBUF + (size_t)z * C::WPLANE;
+        // the slot's previous item must have been read by every consumer
+        if (tg == 0 && s_fwd / NB > 0) sync_wait(&gs->cons[s_fwd % NB], P * (s_fwd / NB));
+        named_bar(2, GT);  // also: pln free for the first exchange copy
+        double2* Wb = c.W + (s_fwd % NB) * C::WBUF + (size_t)z * C::WPLANE;
 #pragma unroll
         for (int ly = 0; ly < N; ++ly) Wb[ly * N + swz(ly, tx)] = cc[ly];
       }
+      named_bar(2, GT);
+      if (tg == 0) {
+        sync_signal(&gs->prod[s_fwd % NB]);
+        issue_load(s_fwd + 1, 0);  // z(0)
+      }
+      seq = s_fwd + 1;
     }
-    cluster_sync_all();
     double q[N];  // gain accumulator of column (tx, tl), then Q
 #pragma unroll
     for (int y = 0; y < N; ++y) q[y] = 0.0;
 #pragma unroll 1
-    for (int k = 0; k <= D + 1; ++k) {
-      TSTAMP(k * 8);
-      if (k >= 2) {
-        const int d = k - 2, pb = d & 1;
-        double2* pln = c.pln0 + pb * C::PSLAB;
-        mbar_wait(c.wbar + pb, (wphase >> pb) & 1u);
-        wphase ^= 1u << pb;
-        TSTAMP(k * 8 + 1);
-        // x pass (rows, in place) then y pass (columns, accumulate): one FFT body for both
-        // passes keeps the hot loop's instruction footprint small.
+    for (int d = 0; d < D; ++d) {
+      TSTAMP(d * 8);
+      const int pb = d & 1;
+      double2* pln = c.pln0 + pb * C::PSLAB;
+      mbar_wait(c.wbar + pb, (wphase >> pb) & 1u);
+      wphase ^= 1u << pb;
+      if (tg == 0) sync_signal(&gs->cons[seq % NB]);  // W(d) read by this CTA
+      TSTAMP(d * 8 + 1);
+      // x pass (rows, in place) then y pass (columns, accumulate): one FFT body for both
+      // passes keeps the hot loop's instruction footprint small.
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-          double2* pl = pln + tl * N * N;  // pass 0: row y = tx; pass 1: column x = tx
-          auto at = [&](int i) { return pass == 0 ? tx * N + swz(tx, i) : i * N + swz(i, tx); };
-          double2 cc[N];
+      for (int pass = 0; pass < 2; ++pass) {
+        double2* pl = pln + tl * N * N;  // pass 0: row y = tx; pass 1: column x = tx
+        auto at = [&](int i) { return pass == 0 ? tx * N + swz(tx, i) : i * N + swz(i, tx); };
+        double2 cc[N];
 #pragma unroll
-          for (int x = 0; x < N; ++x) cc[x] = pl[at(x)];
-          if (pass == 1) named_bar(2, GT);  // plane buffer pb free for the bulk copy of W(k)
-          fft<N, +1>(cc);
-          if (pass == 0) {
+        for (int x = 0; x < N; ++x) cc[x] = pl[at(x)];
+        fft<N, +1>(cc);
+        if (pass == 0) {
 #pragma unroll
-            for (int x = 0; x < N; ++x) pl[at(x)] = cc[x];
-            named_bar(2, GT);
-            TSTAMP(k * 8 + 2);
-          } else if (d < p.A) {
+          for (int x = 0; x < N; ++x) pl[at(x)] = cc[x];
+          named_bar(2, GT);  // rows done; every thread has also finished xy(d-1): buffer pb^1 free
+          if (tg == 0 && d + 1 < D) issue_load(seq + 1, pb ^ 1);
+          TSTAMP(d * 8 + 2);
+        } else if (d < p.A) {
 #pragma unroll
-            for (int y = 0; y < N; ++y) q[y] = fma(cc[y].x, cc[y].y, q[y]);
-          } else if constexpr (C::FS_TMEM) {
+          for (int y = 0; y < N; ++y) q[y] = fma(cc[y].x, cc[y].y, q[y]);
+        } else if constexpr (C::FS_TMEM) {
 #pragma unroll
-            for (int ch = 0; ch < N / 16; ++ch) {
-              double fs[16];
-              fs_chunk(ch, fs);
+          for (int ch = 0; ch < N / 16; ++ch) {
+            double fs[16];
+            fs_chunk(ch, fs);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) q[ch * 16 + i] = q[ch * 16 + i] - fs[i] * cc[ch * 16 + i].x;
-            }  // Q = G - f* c
-          } else {
+            for (int i = 0; i < 16; ++i) q[ch * 16 + i] = q[ch * 16 + i] - fs[i] * cc[ch * 16 + i].x;
+          }  // Q = G - f* c
+        } else {
 #pragma unroll
-            for (int y = 0; y < N; ++y) {
-              const double fs = gather_fstar(p.f_in, p.tp, cc_cell, tx + N * (y + N * z), tx, y, z, n, c.delta);
-              q[y] = q[y] - fs * cc[y].x;  // Q = G - f* c
-            }
+          for (int y = 0; y < N; ++y) {
+            const double fs = gather_fstar(p.f_in, p.tp, cc_cell, tx + N * (y + N * z), tx, y, z, n, c.delta);
+            q[y] = q[y] - fs * cc[y].x;  // Q = G - f* c
           }
         }
-        TSTAMP(k * 8 + 3);
       }
-      // phase k: xy(k-2) done.  The xy group publishes no global writes (it only read W through
-      // completed bulk copies), so no release fence is needed.
-      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
-      TSTAMP(k * 8 + 4);
-      cl_wait();    // W(k) complete everywhere
-      TSTAMP(k * 8 + 5);
-      if (tg == 0 && k < D) {
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        bulk_load(c.pln0 + (k & 1) * C::PSLAB, c.W + (size_t)(k % 4) * C::WBUF + (size_t)rank * C::PSLAB,
-                  kPlaneBytes, c.wbar + (k & 1));
-      }
-      TSTAMP(k * 8 + 6);
+      TSTAMP(d * 8 + 3);
+      ++seq;
     }
     // a8 + a9: projection and Euler (or write Q)
     double* out = p.f_out + cell * (int64_t)n;
@@ -484,7 +514,45 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
           m[3] += vz * q[y];
           m[4] += (vx * vx + vy * vy + vz * vz) * q[y];
         }
-        project_lambda<N, P>(p, c, true, m, lam);
+        // group reduction of the 5 moments in a fixed order (warps, then ranks): deterministic
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
+        }
+        double* wpart = reinterpret_cast<double*>(c.pln0);  // plane buffers idle in the epilogue
+        constexpr int NW = GT / 32;
+        if ((tg & 31) == 0) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) wpart[(tg >> 5) * 5 + k] = m[k];
+        }
+        named_bar(2, GT);
+        double* gpart = gs->partial[ncell & 1][rank];
+        if (tg < 5) {
+          double sum = 0.0;
+          for (int w = 0; w < NW; ++w) sum += wpart[w * 5 + tg];
+          __stcg(gpart + tg, sum);
+        }
+        named_bar(2, GT);
+        if (tg == 0) {
+          sync_signal(&gs->part);
+          sync_wait(&gs->part, P * (ncell + 1));
+          double mu[5] = {0, 0, 0, 0, 0};
+          for (int r = 0; r < P; ++r) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) mu[k] += __ldcg(&gs->partial[ncell & 1][r][k]);
+          }
+#pragma unroll
+          for (int a = 0; a < 5; ++a) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int b = 0; b < 5; ++b) sacc = fma(p.Ginv[a * 5 + b], mu[b], sacc);
+            c.part[a] = sacc;
+          }
+        }
+        named_bar(2, GT);
+#pragma unroll
+        for (int a = 0; a < 5; ++a) lam[a] = c.part[a];
       }
       bool bad = false;
       auto euler = [&](int y, double fs) {
@@ -509,13 +577,8 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
           euler(y, gather_fstar(p.f_in, p.tp, cc_cell, tx + N * (y + N * z), tx, y, z, n, c.delta));
       }
       if (bad) atomicOr(p.nonfinite, 1);
-      if (p.project) {  // part[] is read remotely before it is rewritten (or the CTA exits);
-        // the remote loads completed (their values were consumed), so no release is needed
-        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
-        cl_wait();
-      }
     }
-    __syncthreads();
+    named_bar(2, GT);  // c.part / plane buffers free for the next cell
   }
 }
 
@@ -524,7 +587,6 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   using C = Cfg3<N, P>;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
-  cg::cluster_group cluster = cg::this_cluster();
   Ctx3<N, P> c;
   c.tbuf = reinterpret_cast<double2*>(smem + C::OFF_TBUF);
   c.pln0 = reinterpret_cast<double2*>(smem + C::OFF_PLN);
@@ -534,7 +596,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::OFF_DELTA);
   load_delta(p.tp, sdelta);
   c.delta = sdelta;
-  c.rank = (int)cluster.block_rank();
+  c.rank = (int)(blockIdx.x % P);
   c.cid = blockIdx.x / P;
   c.ncl = gridDim.x / P;
   const int t = threadIdx.x;
@@ -543,6 +605,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.tx = c.tg % N;
   c.tl = c.tg / N;
   c.W = p.scratch + (size_t)c.cid * C::NBUF * C::WBUF;
+  c.gs = reinterpret_cast<GroupSync*>(p.sync) + c.cid;
 
   if (t < 32) {  // warp 0 owns the TMEM allocation
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
@@ -560,91 +623,84 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tbase = *tmem_slot;
-  if (zg) {
-    // this thread's TMEM lane: warp quarter base + lane in warp (row field = bits 31..16)
-    z_group<N, P>(p, c, tbase + ((uint32_t)(32 * ((t >> 5) & 3)) << 16));
-  } else {
-    xy_group<N, P>(p, c, tbase + ((uint32_t)(32 * ((t >> 5) & 3)) << 16));
-  }
+  // this thread's TMEM lane: warp quarter base + lane in warp (row field = bits 31..16)
+  const uint32_t taddr = tbase + ((uint32_t)(32 * ((t >> 5) & 3)) << 16);
+  if (zg) z_group<N, P>(p, c, taddr);
+  else xy_group<N, P>(p, c, taddr);
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(C::TMEM_COLS) : "memory");
 }
 
 template <int N, int P>
-static cudaLaunchConfig_t make_cfg(int nclusters, cudaStream_t s, cudaLaunchAttribute* attr) {
-  using C = Cfg3<N, P>;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nclusters * P);
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = s;
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = P;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cfg;
-}
-
-template <int N, int P>
 static cudaError_t prep() {
   using C = Cfg3<N, P>;
-  auto kern = k_step3d<N, P>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-  if (e != cudaSuccess) return e;
-  if (P > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  return e;
+  return cudaFuncSetAttribute(k_step3d<N, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
 }
 
+// Cooperative launch: all P * ngroups CTAs are co-resident (one per SM), which the group
+// synchronisation through L2 requires.
 template <int N, int P>
-static cudaError_t launch3(const StepParams& p, int nclusters, cudaStream_t s) {
+static cudaError_t launch3(const StepParams& p, int ngroups, cudaStream_t s) {
+  using C = Cfg3<N, P>;
   cudaError_t e = prep<N, P>();
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t cfg = make_cfg<N, P>(nclusters, s, attr);
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ngroups * P);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_step3d<N, P>, p);
 }
 
 template <int N, int P>
-static int max_clusters3() {
+static int max_groups3() {
   if (prep<N, P>() != cudaSuccess) return 0;
-  cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t cfg = make_cfg<N, P>(64, 0, attr);
-  int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, k_step3d<N, P>, &cfg) != cudaSuccess) return 0;
-  return ncl;
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step3d<N, P>, Cfg3<N, P>::THREADS, Cfg3<N, P>::SMEM) !=
+      cudaSuccess)
+    return 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms / P;
 }
 
-// CTAs per cell for N = 32 (8 or 16); 8 for the small grids.  FKS_P32 env var overrides (tuning).
-static int p32() {
-  static int v = [] {
-    const char* e = getenv("FKS_P32");
-    return (e && atoi(e) == 16) ? 16 : 8;
-  }();
-  return v;
-}
-
-cudaError_t launch_step3d(int N, const StepParams& p, int nclusters, cudaStream_t s) {
+cudaError_t launch_step3d(int N, const StepParams& p, int ngroups, cudaStream_t s) {
   switch (N) {
-    case 8: return launch3<8, 2>(p, nclusters, s);
-    case 16: return launch3<16, 8>(p, nclusters, s);
-    case 32: return p32() == 16 ? launch3<32, 16>(p, nclusters, s) : launch3<32, 8>(p, nclusters, s);
+    case 8: return launch3<8, 2>(p, ngroups, s);
+    case 16: return launch3<16, 8>(p, ngroups, s);
+    case 32: return launch3<32, 8>(p, ngroups, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 int max_active_clusters3d(int N) {
   switch (N) {
-    case 8: return max_clusters3<8, 2>();
-    case 16: return max_clusters3<16, 8>();
-    case 32: return p32() == 16 ? max_clusters3<32, 16>() : max_clusters3<32, 8>();
+    case 8: return max_groups3<8, 2>();
+    case 16: return max_groups3<16, 8>();
+    case 32: return max_groups3<32, 8>();
     default: return 0;
   }
 }
 
 size_t scratch_elems3d(int N) { return (size_t)Cfg3<32, 8>::NBUF * N * N * N; }
+
+size_t sync_bytes3d() { return sizeof(GroupSync); }
+
+// Host-side table layout of the 3D kernel for N: T3[p][rank][row][l_x] (see Cfg3::SLABR).
+int table_layout3d(int N, int* P_out, int* NP_out, int* slabr_out) {
+  switch (N) {
+    case 8: *P_out = 2; *NP_out = Cfg3<8, 2>::NP; *slabr_out = Cfg3<8, 2>::SLABR; return 0;
+    case 16: *P_out = 8; *NP_out = Cfg3<16, 8>::NP; *slabr_out = Cfg3<16, 8>::SLABR; return 0;
+    case 32: *P_out = 8; *NP_out = Cfg3<32, 8>::NP; *slabr_out = Cfg3<32, 8>::SLABR; return 0;
+    default: return -1;
+  }
+}
 
 #ifdef FKS_TIMING
 extern "C" int fks_debug_tstamps(long long* out, int count) {
