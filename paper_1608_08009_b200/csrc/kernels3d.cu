@@ -69,10 +69,11 @@ struct Cfg3 {
   static constexpr int USED_COLS = FHAT_COLS + (FS_TMEM ? 2 * N : 0);
   static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
                                  : USED_COLS <= 256 ? 256 : 512;
-  static constexpr size_t OFF_TBUF = 0;
-  static constexpr size_t OFF_PLN = OFF_TBUF + ((size_t)SLAB * 16 + 127) / 128 * 128;  // two plane slabs
-  static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;  // tbar, wbar[2]
-  static constexpr size_t OFF_TMEM = OFF_MBAR + 24;
+  static constexpr size_t TBUF_BYTES = ((size_t)SLAB * 16 + 127) / 128 * 128;
+  static constexpr size_t OFF_TBUF = 0;                       // two table slabs (double-buffered)
+  static constexpr size_t OFF_PLN = OFF_TBUF + 2 * TBUF_BYTES;  // two plane slabs
+  static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;  // tbar[2], wbar[2]
+  static constexpr size_t OFF_TMEM = OFF_MBAR + 32;
   static constexpr size_t OFF_PART = OFF_TMEM + 8;
   static constexpr size_t OFF_DELTA = OFF_PART + 8 * 8;  // int8 [3][kMaxN] shift table
   static constexpr size_t SMEM = OFF_DELTA + 3 * kMaxN;
@@ -229,6 +230,18 @@ __device__ __forceinline__ void sync_signal(unsigned* ctr) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
 }
 
+// Consumer-side signal: the reads it announces have completed (their data is in registers or
+// SMEM), so no ordering is needed and the thread does not wait for a fence.
+__device__ __forceinline__ void sync_signal_relaxed(unsigned* ctr) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* ctr) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* ctr) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
@@ -244,13 +257,23 @@ __device__ __forceinline__ void sync_wait(const unsigned* ctr, unsigned target) 
   }
 }
 
+// Same for a slot that is only going to be overwritten (its readers signalled after their reads
+// completed): a relaxed poll; `seen` is a value loaded earlier, often already sufficient.
+__device__ __forceinline__ void sync_wait_free(const unsigned* ctr, unsigned target, unsigned seen) {
+  unsigned spins = 0;
+  while ((int)(seen - target) < 0) {
+    seen = ld_relaxed(ctr);
+    if (++spins == (1u << 24)) __trap();
+  }
+}
+
 // Shared-memory carve-up and per-thread coordinates of the 3D kernel.
 template <int N, int P>
 struct Ctx3 {
   using C = Cfg3<N, P>;
-  double2* tbuf;   // [NP l_y][N l_z][N l_x] table slab of the current direction
+  double2* tbuf;   // 2 x table slab [SLABR rows][N l_x] (direction g in buffer g & 1)
   double2* pln0;   // 2 x [NP j_z][N y][N x] plane slabs (swizzled)
-  uint64_t* tbar;  // table slab landed
+  uint64_t* tbar;  // [2] table slab landed
   uint64_t* wbar;  // [2] plane slab landed
   double* part;    // [8] epilogue scratch (moment sums, lambda)
   const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
@@ -277,9 +300,25 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
     return (uint32_t)rows * N * 16;
   }();
   const double2* tab_rank = p.tables + (size_t)rank * C::SLAB;  // + direction * P * SLAB
-  uint32_t tphase = 0;
+  // Table stream: direction g % D of the g-th z pass (the tables do not depend on the cell),
+  // slab g in buffer g & 1, loaded two passes ahead.
+  constexpr size_t TB = C::TBUF_BYTES / 16;  // complex elements per table buffer
+  const int my_cells = p.ncells > cid ? (p.ncells - cid + c.ncl - 1) / c.ncl : 0;
+  const int gtotal = my_cells * D;
+  int g = 0;             // z passes done
+  int gload = 0, dload = 0;  // next slab to load and its direction
+  auto load_next = [&]() {  // thread 0
+    if (gload < gtotal)
+      bulk_load(c.tbuf + (gload & 1) * TB, tab_rank + (size_t)dload * P * C::SLAB, kTabBytes, c.tbar + (gload & 1));
+    ++gload;
+    if (++dload == D) dload = 0;
+  };
+  uint32_t tphase = 0;  // bit b: parity of table buffer b
   unsigned seq = 0;  // exchange-buffer sequence index of the next item
-  if (tg == 0) bulk_load(c.tbuf, tab_rank, kTabBytes, c.tbar);
+  if (tg == 0) {
+    load_next();
+    load_next();
+  }
   for (int it = cid; it < p.ncells; it += c.ncl) {
     {  // forward item: the xy transforms of every CTA of the group
       const unsigned slot = seq % NB, use = seq / NB;
@@ -304,7 +343,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       }
       tmem_wait_st();
       named_bar(1, GT);  // every column of the forward item read
-      if (tg == 0) sync_signal(&gs->cons[slot]);
+      if (tg == 0) sync_signal_relaxed(&gs->cons[slot]);
       ++seq;
     }
 #pragma unroll 1
@@ -312,19 +351,19 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       TSTAMP(2048 + j * 8);
       const unsigned slot = seq % NB, use = seq / NB;
       double2 x[N];
-      mbar_wait(c.tbar, tphase);
-      tphase ^= 1;
+      // slot free once its previous item has been read by every consumer (polled early)
+      const unsigned cons_seen = tg == 0 && use > 0 ? ld_relaxed(&gs->cons[slot]) : 0u;
+      const int tb = g & 1;
+      mbar_wait(c.tbar + tb, (tphase >> tb) & 1u);
+      tphase ^= 1u << tb;
       TSTAMP(2048 + j * 8 + 1);
-      zpass_compute<N, P>(taddr, c.tbuf, tx, tm, x);
+      zpass_compute<N, P>(taddr, c.tbuf + tb * TB, tx, tm, x);
       TSTAMP(2048 + j * 8 + 2);
-      // thread 0: slot free (its previous item read by every consumer) before anyone stores
-      if (tg == 0 && use > 0) sync_wait(&gs->cons[slot], P * use);
-      named_bar(1, GT);  // tbuf consumed; the z(j-1) stores of every thread precede this point
+      if (tg == 0 && use > 0) sync_wait_free(&gs->cons[slot], P * use, cons_seen);
+      named_bar(1, GT);  // table buffer tb consumed; the z(j-1) stores of every thread precede this point
+      ++g;
       if (tg == 0) {
-        // next table slab (wrapping to direction 0 of the next cell)
-        const int dn = j + 1 < D ? j + 1 : 0;
-        if (j + 1 < D || it + c.ncl < p.ncells)
-          bulk_load(c.tbuf, tab_rank + (size_t)dn * P * C::SLAB, kTabBytes, c.tbar);
+        load_next();  // slab g + 1 (two passes ahead) into the buffer just freed
         // publish z(j-1): its stores had a whole z pass to drain, so the release is cheap
         if (j > 0) sync_signal(&gs->prod[(seq - 1) % NB]);
       }
@@ -359,9 +398,14 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
 #pragma unroll
     for (int i = 0; i < 16; ++i) fs[i] = __hiloint2double(v[2 * i + 1], v[2 * i]);
   };
-  // thread 0: W(item s) -> plane buffer b, once every producer has published it
-  auto issue_load = [&](unsigned s, int b) {
-    sync_wait(&gs->prod[s % NB], P * (s / NB + 1));
+  // thread 0: W(item s) -> plane buffer b, once every producer has published it (`seen`: an
+  // earlier relaxed read of the counter)
+  auto issue_load = [&](unsigned s, int b, unsigned seen) {
+    const unsigned* ctr = &gs->prod[s % NB];
+    const unsigned target = P * (s / NB + 1);
+    // The producers' release put their stores in L2 before the counter moved, and the bulk copy
+    // reads L2 after the (control-dependent) check, so a relaxed observation is enough here.
+    if ((int)(seen - target) < 0) sync_wait(ctr, target);
     asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic-proxy stores -> bulk reads
     bulk_load(c.pln0 + b * C::PSLAB, c.W + (s % NB) * C::WBUF + (size_t)rank * C::PSLAB, kPlaneBytes, c.wbar + b);
   };
@@ -432,7 +476,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         for (int y = 0; y < N; ++y) cc[y] = col[y * N + swz(y, tx)];
         fft<N, -1>(cc);
         // the slot's previous item must have been read by every consumer
-        if (tg == 0 && s_fwd / NB > 0) sync_wait(&gs->cons[s_fwd % NB], P * (s_fwd / NB));
+        if (tg == 0 && s_fwd / NB > 0) sync_wait_free(&gs->cons[s_fwd % NB], P * (s_fwd / NB), 0u);
         named_bar(2, GT);  // also: pln free for the first exchange copy
         double2* Wb = c.W + (s_fwd % NB) * C::WBUF + (size_t)z * C::WPLANE;
 #pragma unroll
@@ -441,7 +485,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
       named_bar(2, GT);
       if (tg == 0) {
         sync_signal(&gs->prod[s_fwd % NB]);
-        issue_load(s_fwd + 1, 0);  // z(0)
+        issue_load(s_fwd + 1, 0, 0u);  // z(0)
       }
       seq = s_fwd + 1;
     }
@@ -455,7 +499,11 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
       double2* pln = c.pln0 + pb * C::PSLAB;
       mbar_wait(c.wbar + pb, (wphase >> pb) & 1u);
       wphase ^= 1u << pb;
-      if (tg == 0) sync_signal(&gs->cons[seq % NB]);  // W(d) read by this CTA
+      unsigned prod_seen = 0;
+      if (tg == 0) {
+        sync_signal_relaxed(&gs->cons[seq % NB]);  // W(d) read by this CTA
+        if (d + 1 < D) prod_seen = ld_relaxed(&gs->prod[(seq + 1) % NB]);  // checked after pass 0
+      }
       TSTAMP(d * 8 + 1);
       // x pass (rows, in place) then y pass (columns, accumulate): one FFT body for both
       // passes keeps the hot loop's instruction footprint small.
@@ -471,7 +519,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
 #pragma unroll
           for (int x = 0; x < N; ++x) pl[at(x)] = cc[x];
           named_bar(2, GT);  // rows done; every thread has also finished xy(d-1): buffer pb^1 free
-          if (tg == 0 && d + 1 < D) issue_load(seq + 1, pb ^ 1);
+          if (tg == 0 && d + 1 < D) issue_load(seq + 1, pb ^ 1, prod_seen);
           TSTAMP(d * 8 + 2);
         } else if (d < p.A) {
 #pragma unroll
@@ -591,7 +639,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.tbuf = reinterpret_cast<double2*>(smem + C::OFF_TBUF);
   c.pln0 = reinterpret_cast<double2*>(smem + C::OFF_PLN);
   c.tbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
-  c.wbar = c.tbar + 1;
+  c.wbar = c.tbar + 2;
   c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
   int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::OFF_DELTA);
   load_delta(p.tp, sdelta);
@@ -615,6 +663,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   }
   if (t == 0) {
     mbar_init(c.tbar, 1);
+    mbar_init(c.tbar + 1, 1);
     mbar_init(c.wbar, 1);
     mbar_init(c.wbar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
