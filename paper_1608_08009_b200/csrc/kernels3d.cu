@@ -40,8 +40,11 @@ namespace fks {
 #ifdef FKS_TIMING
 __device__ long long g_tstamp[4096];
 #define TSTAMP(slot) do { if (cid == 0 && rank == 0 && (tg == 0) && it == 0) g_tstamp[(slot)] = clock64(); } while (0)
+// cell boundary: the first cell's epilogue and the second cell's forward (slots 1024..)
+#define TSTAMPB(slot) do { if (cid == 0 && rank == 0 && (tg == 0) && (it == 0 || it == c.ncl)) g_tstamp[1024 + (it != 0) * 16 + (slot)] = clock64(); } while (0)
 #else
 #define TSTAMP(slot) do { } while (0)
+#define TSTAMPB(slot) do { } while (0)
 #endif
 
 template <int N, int P>
@@ -65,20 +68,24 @@ struct Cfg3 {
   static constexpr int FHAT_COLS = 4 * N;     // one f^ pencil (N complex fp64) per lane (z group)
   // f* column cache (xy group, N >= 16): column (l_x = tx, j_z) of f* (N fp64 = 2N columns),
   // read back by the loss term and the Euler update instead of re-gathering f from HBM.
-  static constexpr bool FS_TMEM = N >= 16;
-  static constexpr int USED_COLS = FHAT_COLS + (FS_TMEM ? 2 * N : 0);
+  // The z group writes it, so z warp w and xy warp w + 4 must share a TMEM lane quarter (GT = 128).
+  static constexpr bool FS_TMEM = N >= 16 && N * (N / P) == 128;
+  static constexpr int USED_COLS = FHAT_COLS + (FS_TMEM ? 2 * 2 * N : 0);  // two cache parities
   static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
                                  : USED_COLS <= 256 ? 256 : 512;
   static constexpr size_t TBUF_BYTES = ((size_t)SLAB * 16 + 127) / 128 * 128;
   static constexpr size_t OFF_TBUF = 0;                       // two table slabs (double-buffered)
   static constexpr size_t OFF_PLN = OFF_TBUF + 2 * TBUF_BYTES;  // two plane slabs
-  static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;  // tbar[2], wbar[2]
-  static constexpr size_t OFF_TMEM = OFF_MBAR + 32;
-  static constexpr size_t OFF_PART = OFF_TMEM + 8;
-  static constexpr size_t OFF_DELTA = OFF_PART + 8 * 8;  // int8 [3][kMaxN] shift table
+  // mbarriers: tbar[2], wbar[2], fsb[2] (f* cache written), fse[2] (f* cache read)
+  static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;
+  static constexpr size_t OFF_TMEM = OFF_MBAR + 64;
+  static constexpr size_t OFF_PART = OFF_TMEM + 8;           // lambda[5] + warp partials [4][5]
+  static constexpr size_t OFF_DELTA = OFF_PART + 32 * 8;  // int8 [3][kMaxN] shift table
   static constexpr size_t SMEM = OFF_DELTA + 3 * kMaxN;
   static_assert(GT % 32 == 0, "warp groups must be whole warps");
   static_assert(NP % 2 == 0, "mirror pairs stay within a CTA");
+  static_assert(2 * ((SLAB * 16 + 127) / 128 * 128) >= (size_t)NP * N * N * 16,
+                "the two table buffers hold one plane slab (z-group forward)");
   static_assert(GT <= 128, "one TMEM lane per z-group thread");
   static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM allocation: power of two >= 32");
 };
@@ -109,6 +116,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
@@ -275,6 +286,8 @@ struct Ctx3 {
   double2* pln0;   // 2 x [NP j_z][N y][N x] plane slabs (swizzled)
   uint64_t* tbar;  // [2] table slab landed
   uint64_t* wbar;  // [2] plane slab landed
+  uint64_t* fsb;   // [2] f* cache of parity b written (z group, GT arrivals)
+  uint64_t* fse;   // [2] f* cache of parity b read for the last time (xy group, GT arrivals)
   double* part;    // [8] epilogue scratch (moment sums, lambda)
   const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
   double2* W;      // [NBUF][N j_z][N l_y][N l_x] exchange buffers of this group (L2, swizzled)
@@ -282,7 +295,12 @@ struct Ctx3 {
   int rank, cid, ncl, tg, tx, tl;
 };
 
-// ---- z group: forward z-FFT into TMEM, then z(j) for every direction ----------------------
+// ---- z group: per cell the forward transform, then z(j) for every direction --------------
+// Forward (a3 + a4): this CTA's j_z planes of f* are gathered into the table buffers (idle
+// between cells), transformed along x and y and published as the forward item; the f* column
+// (tx, ., j_z) goes to the xy thread's TMEM lane (cache parity = cell parity).  Then the z
+// transform of the CTA's l_y pencils (the forward item of every CTA) into TMEM, and the z passes.
+// Doing the forward here lets it overlap the xy group's last directions and epilogue.
 template <int N, int P>
 __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c, uint32_t taddr) {
   using C = Cfg3<N, P>;
@@ -300,29 +318,107 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
     return (uint32_t)rows * N * 16;
   }();
   const double2* tab_rank = p.tables + (size_t)rank * C::SLAB;  // + direction * P * SLAB
-  // Table stream: direction g % D of the g-th z pass (the tables do not depend on the cell),
-  // slab g in buffer g & 1, loaded two passes ahead.
   constexpr size_t TB = C::TBUF_BYTES / 16;  // complex elements per table buffer
-  const int my_cells = p.ncells > cid ? (p.ncells - cid + c.ncl - 1) / c.ncl : 0;
-  const int gtotal = my_cells * D;
-  int g = 0;             // z passes done
-  int gload = 0, dload = 0;  // next slab to load and its direction
-  auto load_next = [&]() {  // thread 0
-    if (gload < gtotal)
-      bulk_load(c.tbuf + (gload & 1) * TB, tab_rank + (size_t)dload * P * C::SLAB, kTabBytes, c.tbar + (gload & 1));
-    ++gload;
-    if (++dload == D) dload = 0;
+  auto load_tab = [&](int j) {  // thread 0: direction j -> table buffer j & 1
+    bulk_load(c.tbuf + (j & 1) * TB, tab_rank + (size_t)j * P * C::SLAB, kTabBytes, c.tbar + (j & 1));
   };
   uint32_t tphase = 0;  // bit b: parity of table buffer b
-  unsigned seq = 0;  // exchange-buffer sequence index of the next item
-  if (tg == 0) {
-    load_next();
-    load_next();
-  }
-  for (int it = cid; it < p.ncells; it += c.ncl) {
-    {  // forward item: the xy transforms of every CTA of the group
-      const unsigned slot = seq % NB, use = seq / NB;
+  unsigned seq = 0;     // exchange-buffer sequence index of the next item
+  unsigned ncell = 0;   // cells done by this group
+  for (int it = cid; it < p.ncells; it += c.ncl, ++ncell) {
+    const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    const CellCoord cc_cell = cell_coord(p.tp, cell);
+    const int zpl = rank * NP + tl;  // forward: this thread's j_z plane
+    const unsigned par = ncell & 1;
+    const uint32_t fs_addr = taddr + C::FHAT_COLS + par * 2 * N;  // xy lane's f* cache (same lane)
+    // this CTA's planes of the next cell (homogeneous case: contiguous) -> L2
+    if (p.tp.dx == 0 && tg == 0 && !p.cell_list && it + c.ncl < p.ncells)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.f_in + (int64_t)(it + c.ncl) * n +
+                                                                        (int64_t)rank * NP * N * N),
+                   "r"((uint32_t)(NP * N * N * sizeof(double)))
+                   : "memory");
+    const unsigned s_fwd = seq;
+    TSTAMPB(0);
+    {  // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[s_fwd % NB]
+      double2* pln = c.tbuf;  // both table buffers: one plane slab
+      constexpr int PER = NP * N * N / GT;  // = N elements per thread
+      constexpr int B = PER < 16 ? PER : 16;
+#pragma unroll 1
+      for (int b0 = 0; b0 < PER; b0 += B) {
+        double v[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int e = tg + (b0 + j) * GT;
+          const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
+          v[j] = gather_fstar(p.f_in, p.tp, cc_cell, x + N * (y + N * zz), x, y, zz, n, c.delta);
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int e = tg + (b0 + j) * GT;
+          const int x = e % N, y = (e / N) % N, zl = e / (N * N);
+          pln[zl * N * N + y * N + swz(y, x)] = make_double2(v[j], 0.0);
+        }
+      }
+      named_bar(1, GT);
+      if constexpr (C::FS_TMEM) {  // column (tx, ., tl) of f* -> the xy thread's TMEM cache
+        if (ncell >= 2) {           // the xy group has finished with this parity (cell ncell - 2)
+          mbar_wait(c.fse + par, ((ncell >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        }
+        const double2* col = pln + tl * N * N;
+#pragma unroll
+        for (int ch = 0; ch < N / 16; ++ch) {
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int y = ch * 16 + i;
+            const double f = col[y * N + swz(y, tx)].x;
+            v[2 * i] = __double2loint(f);
+            v[2 * i + 1] = __double2hiint(f);
+          }
+          tmem_st32(fs_addr + ch * 32, v);
+        }
+        tmem_wait_st();
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        mbar_arrive(c.fsb + par);
+        named_bar(1, GT);  // every column read before the rows are transformed in place
+      }
+      {
+        double2 r[N];
+        double2* row = pln + tl * N * N + tx * N;  // row y = tx of plane tl
+#pragma unroll
+        for (int x = 0; x < N; ++x) r[x] = row[swz(tx, x)];
+        fft<N, -1>(r);
+#pragma unroll
+        for (int x = 0; x < N; ++x) row[swz(tx, x)] = r[x];
+        TSTAMPB(1);
+      }
+      named_bar(1, GT);
+      {
+        double2 cc[N];
+        const double2* col = pln + tl * N * N;  // column l_x = tx of plane tl
+#pragma unroll
+        for (int y = 0; y < N; ++y) cc[y] = col[y * N + swz(y, tx)];
+        fft<N, -1>(cc);
+        // the slot's previous item must have been read by every consumer
+        if (tg == 0 && s_fwd / NB > 0) sync_wait_free(&gs->cons[s_fwd % NB], P * (s_fwd / NB), 0u);
+        named_bar(1, GT);  // also: every plane read, the table buffers may be refilled
+        if (tg == 0) {
+          load_tab(0);
+          if (D > 1) load_tab(1);
+        }
+        double2* Wb = c.W + (s_fwd % NB) * C::WBUF + (size_t)zpl * C::WPLANE;
+#pragma unroll
+        for (int l = 0; l < N; ++l) Wb[l * N + swz(l, tx)] = cc[l];
+      }
+      named_bar(1, GT);
+      if (tg == 0) sync_signal(&gs->prod[s_fwd % NB]);
+      TSTAMPB(2);
+    }
+    {  // z transform of the forward item of every CTA -> f^ pencil in TMEM
+      const unsigned slot = s_fwd % NB, use = s_fwd / NB;
       if (tg == 0) sync_wait(&gs->prod[slot], P * (use + 1));
+      TSTAMPB(9);
       named_bar(1, GT);
       double2 x[N];
       const double2* Wb = c.W + slot * C::WBUF + (size_t)ly * N + swz(ly, tx);
@@ -343,8 +439,9 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       }
       tmem_wait_st();
       named_bar(1, GT);  // every column of the forward item read
+      TSTAMPB(10);
       if (tg == 0) sync_signal_relaxed(&gs->cons[slot]);
-      ++seq;
+      seq = s_fwd + 1;
     }
 #pragma unroll 1
     for (int j = 0; j < D; ++j) {
@@ -353,7 +450,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       double2 x[N];
       // slot free once its previous item has been read by every consumer (polled early)
       const unsigned cons_seen = tg == 0 && use > 0 ? ld_relaxed(&gs->cons[slot]) : 0u;
-      const int tb = g & 1;
+      const int tb = j & 1;
       mbar_wait(c.tbar + tb, (tphase >> tb) & 1u);
       tphase ^= 1u << tb;
       TSTAMP(2048 + j * 8 + 1);
@@ -361,9 +458,8 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       TSTAMP(2048 + j * 8 + 2);
       if (tg == 0 && use > 0) sync_wait_free(&gs->cons[slot], P * use, cons_seen);
       named_bar(1, GT);  // table buffer tb consumed; the z(j-1) stores of every thread precede this point
-      ++g;
       if (tg == 0) {
-        load_next();  // slab g + 1 (two passes ahead) into the buffer just freed
+        if (j + 2 < D) load_tab(j + 2);  // into the buffer just freed
         // publish z(j-1): its stores had a whole z pass to drain, so the release is cheap
         if (j > 0) sync_signal(&gs->prod[(seq - 1) % NB]);
       }
@@ -371,12 +467,12 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       TSTAMP(2048 + j * 8 + 3);
       ++seq;
     }
-    named_bar(1, GT);  // the z(D-1) stores of every thread precede the release
+    named_bar(1, GT);  // the z(D-1) stores of every thread precede the release; tables consumed
     if (tg == 0) sync_signal(&gs->prod[(seq - 1) % NB]);
   }
 }
 
-// ---- xy group: forward x/y FFT, then xy(j) and the gain accumulation, epilogue -------------
+// ---- xy group: xy(j) and the gain accumulation, epilogue ---------------------------------
 template <int N, int P>
 __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& c, uint32_t taddr) {
   using C = Cfg3<N, P>;
@@ -389,15 +485,6 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
   uint32_t wphase = 0;  // bit b = parity of plane buffer b
   unsigned seq = 0;     // exchange-buffer sequence index of the next item
   unsigned ncell = 0;   // cells done by this group
-  const uint32_t saddr = taddr + C::FHAT_COLS;  // f* column cache (FS_TMEM)
-  // f*(tx, y, z) for y in [16 ch, 16 ch + 16) from the column cache
-  auto fs_chunk = [&](int ch, double (&fs)[16]) {
-    uint32_t v[32];
-    tmem_ld32(saddr + ch * 32, v);
-    tmem_wait_ld();
-#pragma unroll
-    for (int i = 0; i < 16; ++i) fs[i] = __hiloint2double(v[2 * i + 1], v[2 * i]);
-  };
   // thread 0: W(item s) -> plane buffer b, once every producer has published it (`seen`: an
   // earlier relaxed read of the counter)
   auto issue_load = [&](unsigned s, int b, unsigned seen) {
@@ -413,82 +500,31 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
     const CellCoord cc_cell = cell_coord(p.tp, cell);
     const int z = rank * NP + tl;
-    // this CTA's planes of the next cell (homogeneous case: contiguous) -> L2
-    if (p.tp.dx == 0 && tg == 0 && !p.cell_list && it + c.ncl < p.ncells)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.f_in + (int64_t)(it + c.ncl) * n +
-                                                                        (int64_t)rank * NP * N * N),
-                   "r"((uint32_t)(NP * N * N * sizeof(double)))
-                   : "memory");
-    const unsigned s_fwd = seq;
-    // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[s_fwd % NB]
-    {
-      double2* pln = c.pln0;
-      constexpr int PER = NP * N * N / GT;  // = N elements per thread
-      constexpr int B = PER < 16 ? PER : 16;
-#pragma unroll 1
-      for (int b0 = 0; b0 < PER; b0 += B) {
-        double v[B];
+    const unsigned par = ncell & 1;
+    const uint32_t saddr = taddr + C::FHAT_COLS + par * 2 * N;  // f* column cache of this cell
+    // f*(tx, y, z) for y in [16 ch, 16 ch + 16) from the column cache
+    auto fs_chunk = [&](int ch, double (&fs)[16]) {
+      uint32_t v[32];
+      tmem_ld32(saddr + ch * 32, v);
+      tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < B; ++j) {
-          const int e = tg + (b0 + j) * GT;
-          const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
-          v[j] = gather_fstar(p.f_in, p.tp, cc_cell, x + N * (y + N * zz), x, y, zz, n, c.delta);
-        }
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          const int e = tg + (b0 + j) * GT;
-          const int x = e % N, y = (e / N) % N, zl = e / (N * N);
-          pln[zl * N * N + y * N + swz(y, x)] = make_double2(v[j], 0.0);
-        }
+      for (int i = 0; i < 16; ++i) fs[i] = __hiloint2double(v[2 * i + 1], v[2 * i]);
+    };
+    auto fs_acquire = [&]() {  // the z group wrote this cell's f* cache
+      if constexpr (C::FS_TMEM) {
+        mbar_wait(c.fsb + par, (ncell >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       }
-      named_bar(2, GT);
-      if constexpr (C::FS_TMEM) {  // column (tx, ., tl) of f* -> TMEM cache
-        const double2* col = pln + tl * N * N;
-#pragma unroll
-        for (int ch = 0; ch < N / 16; ++ch) {
-          uint32_t v[32];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int y = ch * 16 + i;
-            const double f = col[y * N + swz(y, tx)].x;
-            v[2 * i] = __double2loint(f);
-            v[2 * i + 1] = __double2hiint(f);
-          }
-          tmem_st32(saddr + ch * 32, v);
-        }
-        tmem_wait_st();
-        named_bar(2, GT);  // every column read before the rows are transformed in place
+    };
+    auto fs_release = [&]() {  // last read of this cell's f* cache done
+      if constexpr (C::FS_TMEM) {
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        mbar_arrive(c.fse + par);
       }
-      {
-        double2 r[N];
-        double2* row = pln + tl * N * N + tx * N;  // row y = tx of plane tl
-#pragma unroll
-        for (int x = 0; x < N; ++x) r[x] = row[swz(tx, x)];
-        fft<N, -1>(r);
-#pragma unroll
-        for (int x = 0; x < N; ++x) row[swz(tx, x)] = r[x];
-      }
-      named_bar(2, GT);
-      {
-        double2 cc[N];
-        const double2* col = pln + tl * N * N;  // column l_x = tx of plane tl
-#pragma unroll
-        for (int y = 0; y < N; ++y) cc[y] = col[y * N + swz(y, tx)];
-        fft<N, -1>(cc);
-        // the slot's previous item must have been read by every consumer
-        if (tg == 0 && s_fwd / NB > 0) sync_wait_free(&gs->cons[s_fwd % NB], P * (s_fwd / NB), 0u);
-        named_bar(2, GT);  // also: pln free for the first exchange copy
-        double2* Wb = c.W + (s_fwd % NB) * C::WBUF + (size_t)z * C::WPLANE;
-#pragma unroll
-        for (int ly = 0; ly < N; ++ly) Wb[ly * N + swz(ly, tx)] = cc[ly];
-      }
-      named_bar(2, GT);
-      if (tg == 0) {
-        sync_signal(&gs->prod[s_fwd % NB]);
-        issue_load(s_fwd + 1, 0, 0u);  // z(0)
-      }
-      seq = s_fwd + 1;
-    }
+    };
+    seq += 1;  // the forward item (z group's)
+    TSTAMPB(3);
+    if (tg == 0) issue_load(seq, 0, 0u);  // z(0): both plane buffers are free here
     double q[N];  // gain accumulator of column (tx, tl), then Q
 #pragma unroll
     for (int y = 0; y < N; ++y) q[y] = 0.0;
@@ -525,6 +561,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
 #pragma unroll
           for (int y = 0; y < N; ++y) q[y] = fma(cc[y].x, cc[y].y, q[y]);
         } else if constexpr (C::FS_TMEM) {
+          fs_acquire();
 #pragma unroll
           for (int ch = 0; ch < N / 16; ++ch) {
             double fs[16];
@@ -543,9 +580,11 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
       TSTAMP(d * 8 + 3);
       ++seq;
     }
+    TSTAMPB(4);
     // a8 + a9: projection and Euler (or write Q)
     double* out = p.f_out + cell * (int64_t)n;
     if (p.mode == 0) {
+      fs_release();
 #pragma unroll
       for (int y = 0; y < N; ++y) out[tx + N * (y + N * z)] = q[y];
     } else {
@@ -568,7 +607,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
         }
-        double* wpart = reinterpret_cast<double*>(c.pln0);  // plane buffers idle in the epilogue
+        double* wpart = c.part + 8;  // [NW][5]
         constexpr int NW = GT / 32;
         if ((tg & 31) == 0) {
 #pragma unroll
@@ -583,6 +622,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         }
         named_bar(2, GT);
         if (tg == 0) {
+          TSTAMPB(5);
           sync_signal(&gs->part);
           sync_wait(&gs->part, P * (ncell + 1));
           double mu[5] = {0, 0, 0, 0, 0};
@@ -599,6 +639,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
           }
         }
         named_bar(2, GT);
+        TSTAMPB(6);
 #pragma unroll
         for (int a = 0; a < 5; ++a) lam[a] = c.part[a];
       }
@@ -619,6 +660,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
 #pragma unroll
           for (int i = 0; i < 16; ++i) euler(ch * 16 + i, fs[i]);
         }
+        fs_release();
       } else {
 #pragma unroll
         for (int y = 0; y < N; ++y)
@@ -627,6 +669,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
       if (bad) atomicOr(p.nonfinite, 1);
     }
     named_bar(2, GT);  // c.part / plane buffers free for the next cell
+    TSTAMPB(7);
   }
 }
 
@@ -640,6 +683,8 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.pln0 = reinterpret_cast<double2*>(smem + C::OFF_PLN);
   c.tbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
   c.wbar = c.tbar + 2;
+  c.fsb = c.tbar + 4;
+  c.fse = c.tbar + 6;
   c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
   int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::OFF_DELTA);
   load_delta(p.tp, sdelta);
@@ -666,6 +711,10 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
     mbar_init(c.tbar + 1, 1);
     mbar_init(c.wbar, 1);
     mbar_init(c.wbar + 1, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(c.fsb + i, C::GT);
+      mbar_init(c.fse + i, C::GT);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

@@ -35,3 +35,11 @@ if ts[3072 + 8]:
         v = ts[3072 + g * 8:3072 + g * 8 + 8]
         if v[0] or v[3]:
             print(g, " ".join(f"{(x - base) if x else -1:7d}" for x in v))
+names = ["z fwd start", "z fwd rows done", "z fwd W stored+signalled", "xy cell start (load z(0))", "xy epilogue start",
+         "xy partials ready", "xy lambda ready", "xy cell done", "-", "z fwd available", "z fwd read+FFT done"]
+print("cell boundary (cell 0 epilogue = first set; cell 1 forward = second set)")
+for c in range(2):
+    for i, nm in enumerate(names):
+        v = ts[1024 + c * 16 + i]
+        if v:
+            print(f"  cell{c} {nm:24s} {v - base:8d}")
