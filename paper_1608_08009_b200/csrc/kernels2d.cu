@@ -195,58 +195,62 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
     const int tcol = neg ? N - tx : tx;
 #pragma unroll 1
     for (int d = 0; d <= p.A; ++d) {
-      {
+      // pass 0: column l_x = tx, X = T f^ from TMEM, IFFT along y -> work plane;
+      // pass 1: row j_y = tx from the work plane, IFFT along x, accumulate.  One FFT body for
+      // both passes halves the loop's instruction footprint (instruction-cache misses were the
+      // top stall reason of the two-body loop, profiles/r01_ncu_k_step2d.json).
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
         double2 c[N];
+        if (pass == 0) {
 #pragma unroll
-        for (int ch = 0; ch < N / 8; ++ch) {
-          uint32_t v[32];
-          tmem2_ld32(taddr + ch * 32, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          for (int ch = 0; ch < N / 8; ++ch) {
+            uint32_t v[32];
+            tmem2_ld32(taddr + ch * 32, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int ly = ch * 8 + i;
-            double2 t;
-            if (TAB_SMEM) {
-              const int row = neg ? (N - ly) & (N - 1) : ly;
-              t = tab[((size_t)d * N + row) * HC + tcol];
-            } else {
-              t = __ldg(p.tables + (size_t)d * n + ly * N + tx);
+            for (int i = 0; i < 8; ++i) {
+              const int ly = ch * 8 + i;
+              double2 t;
+              if (TAB_SMEM) {
+                const int row = neg ? (N - ly) & (N - 1) : ly;
+                t = tab[((size_t)d * N + row) * HC + tcol];
+              } else {
+                t = __ldg(p.tables + (size_t)d * n + ly * N + tx);
+              }
+              const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
+              const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
+              c[ly] = make_double2(fma(t.x, Fx, -t.y * Fy), fma(t.x, Fy, t.y * Fx));
             }
-            const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
-            const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
-            c[ly] = make_double2(fma(t.x, Fx, -t.y * Fy), fma(t.x, Fy, t.y * Fx));
           }
+        } else {
+#pragma unroll
+          for (int x = 0; x < N; ++x) c[x] = wk[tx * N + swz2(tx, x)];
         }
         fft<N, +1>(c);
+        if (pass == 0) {
 #pragma unroll
-        for (int y = 0; y < N; ++y) wk[y * N + swz2(y, tx)] = c[y];
-      }
-      __syncwarp(mask);
-      {
-        double2 r[N];
+          for (int y = 0; y < N; ++y) wk[y * N + swz2(y, tx)] = c[y];
+        } else if (d < p.A) {
 #pragma unroll
-        for (int x = 0; x < N; ++x) r[x] = wk[tx * N + swz2(tx, x)];
-        fft<N, +1>(r);
-        if (d < p.A) {
-#pragma unroll
-          for (int x = 0; x < N; ++x) gacc[x] = fma(r[x].x, r[x].y, gacc[x]);
+          for (int x = 0; x < N; ++x) gacc[x] = fma(c[x].x, c[x].y, gacc[x]);
         } else if constexpr (C::FS_TMEM) {
 #pragma unroll
           for (int ch = 0; ch < N / 16; ++ch) {
             double fs[16];
             fs_chunk(ch, fs);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) gacc[ch * 16 + i] = gacc[ch * 16 + i] - fs[i] * r[ch * 16 + i].x;
+            for (int i = 0; i < 16; ++i) gacc[ch * 16 + i] = gacc[ch * 16 + i] - fs[i] * c[ch * 16 + i].x;
           }  // gacc now holds Q
         } else {
 #pragma unroll
           for (int x = 0; x < N; ++x) {
             const double fs = gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta);
-            gacc[x] = gacc[x] - fs * r[x].x;  // gacc now holds Q
+            gacc[x] = gacc[x] - fs * c[x].x;  // gacc now holds Q
           }
         }
+        __syncwarp(mask);
       }
-      __syncwarp(mask);
     }
     double* out = p.f_out + cell * (int64_t)n;
     const double* q = gacc;
