@@ -22,7 +22,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "collision evals/s (Nv=32³, M dirs) and phase-space updates/s at 1/2/4/8 B200"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-NCU_SUMMARY = {3: os.path.join(ROOT, "profiles", "r01_ncu_k_step3d.json")}
+NCU_SUMMARY = {3: os.path.join(ROOT, "profiles", "r01_ncu_k_step3d.json"),
+               2: os.path.join(ROOT, "profiles", "r01_ncu_k_step2d.json")}
 
 
 def dram_traffic(dv, ncells):
@@ -333,7 +334,8 @@ def main():
             "phase_space_updates_per_s": value * n,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": dram_traffic(dv, ncells),
-                         "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01_ncu_k_step3d.json)",
+                         "traffic_unit": "bytes per launch (ncu dram read+write per cell x cells, "
+                                         f"{os.path.relpath(NCU_SUMMARY[dv], ROOT)})",
                          "algorithmic_bytes": 2 * n * 8 * ncells,
                          "kernel": "k_step3d" if dv == 3 else "k_step2d",
                          "flops_per_cell": fl, "kernel_ms_avg": kern_avg_ms,
