@@ -1,33 +1,25 @@
 // 3D fused collision / step kernel (a3-a9) for hard spheres on an N^3 velocity grid.
 //
-// One thread-block cluster of P CTAs owns one cell at a time (persistent over cells).  The
-// cell's N^3 spectrum does not fit one SM (N = 32: 512 KiB per complex transform), so the
-// 3D inverse FFT of each direction is split by planes:
-//   CTA r owns the spectrum planes l_y in [r N/P, (r+1) N/P)  (f^ resident in SMEM) and
-//   the output planes  j_z in [r N/P, (r+1) N/P)             (gain accumulator in registers).
+// A group of P co-resident CTAs (cooperative launch, one CTA per SM) owns one cell at a time,
+// persistent over cells.  The cell's N^3 spectrum does not fit one SM (N = 32: 512 KiB per
+// complex transform), so the 3D inverse FFT of each direction is split by planes:
+//   CTA r owns NP = N/P spectrum planes l_y (mirror pairs l_y, -l_y; f^ resident in TMEM) and
+//   the output planes j_z in [r NP, (r+1) NP) (gain accumulator in registers).
 // Per direction p the CTA
-//   z: forms X = (alpha~_p + i alpha'~_p) f^ on its pencils and IFFTs along z in registers,
-//      then writes the pencils to a per-cluster L2 exchange buffer (the transpose);
-//   xy: after a cluster barrier, bulk-copies its own j_z planes back (cp.async.bulk, async
-//      proxy), IFFTs along x and y and accumulates G += Re z * Im z -- two real transforms
-//      packed in one complex IFFT, exact because the symmetrised tables are real and even
-//      (reading #10).
-// Warp specialisation and pipeline (per cell, D = A + 1 exchanges, the loss is the last one,
-// with table (D~, 0)).  The CTA has a z group and an xy group of N*NP threads each; phase k of
-// the cluster barrier completes when every z group has stored z(k) and every xy group has
-// finished xy(k-2):
-//   z group : arrive k; compute z(k+1) in registers (overlaps the barrier); wait k; store z(k+1)
-//   xy group: xy(k-2) from plane buffer (k-2)%2; arrive k; wait k; bulk-copy W(k) -> buffer k%2
-// so every exchange copy lands while the previous direction is being transformed, and the
-// z group's FFT overlaps the barrier.  Three exchange buffers per cluster.  The per-cell f^
-// slab lives in tensor memory (TMEM, 128 columns x 128 lanes: one pencil per z-group lane,
-// tcgen05.st / tcgen05.ld), which frees shared memory for the double-buffered plane slabs and
-// the bulk-prefetched table slab.  The exchange goes through L2 (measured ~15 TB/s) rather than
-// DSMEM (measured ~2 TB/s, profiles/r01_microbench.txt).  Epilogue: Q = G - f* Re z(loss),
-// projection to zero moments (5-sum cluster reduction through DSMEM) and
+//   z group : forms X = (alpha~_p + i alpha'~_p) f^ on its pencils and IFFTs along z in
+//             registers, then writes the pencils to the group's L2 exchange ring (the transpose);
+//   xy group: bulk-copies its own j_z planes back (cp.async.bulk, async proxy), IFFTs along x and
+//             y and accumulates G += Re z * Im z -- two real transforms packed in one complex
+//             IFFT, exact because the symmetrised tables are real and even (reading #10).
+// The loss is the (A+1)-th exchange with table (D~, 0); Q = G - f* Re z(loss),
+// projection to zero moments (5-sum group reduction through L2) and
 // F^{n+1} = f* + (dt/tau) Pi Q, or Q in collide mode.
+// Synchronisation is by per-group counters in L2 (GroupSync below), not cluster barriers: the z
+// group runs up to NBUF-1 exchange items ahead of the xy group and computes the next cell's
+// forward transform (a3 + a4) while the xy group finishes the previous cell.  The exchange goes
+// through L2 (bulk reads ~54 B/clk/SM) rather than DSMEM (~7 B/clk/SM, profiles/r01_microbench.txt).
 // Tables are pre-folded on the host: alpha~ = s w_p alpha_p / n, alpha'~ = alpha'_p / n,
-// D~ = s D / n (s = Btilde kappa^-(d+gamma)); layout T[p][l_y][l_z][l_x] as double2.
+// D~ = s D / n (s = Btilde kappa^-(d+gamma)); layout T3[p][rank][row][l_x] (Cfg3::SLABR).
 #include <cstdlib>
 
 #include "common.cuh"
