@@ -26,6 +26,15 @@ NCU_SUMMARY = {3: os.path.join(ROOT, "profiles", "r01_ncu_k_step3d.json"),
                2: os.path.join(ROOT, "profiles", "r01_ncu_k_step2d.json")}
 
 
+def hbm_peak():
+    """Measured HBM copy bandwidth (GB/s) from MEASURED_PEAKS.json, else the guide's fallback."""
+    try:
+        with open(PEAKS) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 7700.0
+
+
 def dram_traffic(dv, ncells):
     """dram__bytes_read + dram__bytes_write per launch from the committed `ncu --set full` capture
     of the dominant kernel (per-cell figure x cells of this launch), or None."""
@@ -273,6 +282,33 @@ def main():
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
     achieved = fl * nfluid_local / (kern_avg_ms * 1e-3) / 1e12
 
+    # ---- secondary figures (not the headline): collide-only and transport-only rates ---------
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    extra = {}
+    if stepper is None:
+        reps = max(1, min(a.steps, 5))
+        ms_c = timed(lambda: ctx.collide(fa, fb), reps)
+        extra["collide_only"] = {"value": nfluid_local / (ms_c * 1e-3), "unit": "cells/s", "ms": ms_c,
+                                 "what": "fks_collide (a4-a7, Q only), same cells"}
+        if c["dx_dim"] > 0:
+            ms_t = timed(lambda: ctx.transport(fa, fb, dt), reps)
+            gbs = 2 * ncells * n * 8 / (ms_t * 1e-3) / 1e9
+            peak = hbm_peak()
+            extra["transport_only"] = {"value": ncells / (ms_t * 1e-3), "unit": "cells/s", "ms": ms_t,
+                                       "hbm_gbs": gbs, "hbm_peak_gbs": peak,
+                                       "hbm_frac": gbs / peak if peak else None,
+                                       "what": "fks_transport (a1+a3, 16 B per phase-space update), HBM-bound"}
+        ctx.check()
+
     # ---- e2e through the C ABI with host buffers (H2D + step + D2H per step) --------------
     e2e = None
     if not a.no_e2e and F is not None and stepper is None:
@@ -337,11 +373,13 @@ def main():
                          "traffic_unit": "bytes per launch (ncu dram read+write per cell x cells, "
                                          f"{os.path.relpath(NCU_SUMMARY[dv], ROOT)})",
                          "algorithmic_bytes": 2 * n * 8 * ncells,
+                         "hbm_frac": (2 * n * 8 * nfluid_local / (kern_avg_ms * 1e-3) / 1e9) / hbm_peak(),
                          "kernel": "k_step3d" if dv == 3 else "k_step2d",
                          "flops_per_cell": fl, "kernel_ms_avg": kern_avg_ms,
                          "note": "FP64 DFMA peak 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured 37.1); "
                                  "flops in the 5 n log2 n FFT convention (SURVEY App. A.9)"},
             "gpu_launches": launches,
+            "secondary": extra,
             "clocks": clk,
             "cpu_baseline": cpu,
             "e2e": e2e,
