@@ -65,18 +65,19 @@ __device__ __forceinline__ CellCoord cell_coord(const TransportParams& tp, int64
 // of the paper's z-slab decomposition (Fig. mpi-decomp).
 // delta: the shift table [3][kMaxN] (a shared-memory copy of tp.delta in the hot kernels: its
 // index varies across a warp, which serialises constant-bank loads).
-__device__ __forceinline__ double gather_fstar(const double* __restrict__ F, const TransportParams& tp,
-                                               const CellCoord& cc, int k, int kx, int ky, int kz, int n,
-                                               const int8_t (*delta)[kMaxN]) {
-  if (tp.dx == 0) return F[cc.cell * n + k];
-  const int kc[3] = {kx, ky, kz};
+// Where f*_cell reads velocity k from when the per-axis shifts of k are d[a] (a < tp.dx): the
+// returned base satisfies f*_cell[k] = base[k] -- the source cell's vector, a ghost vector or a
+// halo plane (the rules of gather_fstar below).
+__device__ __forceinline__ const double* source_base(const double* __restrict__ F, const TransportParams& tp,
+                                                     const CellCoord& cc, const int (&d)[3], int n) {
+  if (tp.dx == 0) return F + cc.cell * n;
   int64_t src = 0, stride = 1, hplane = 0;
   int gface = -1;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     if (a < tp.dx) {
       const int Ma = tp.M[a];
-      int s = cc.j[a] + delta[a][kc[a]];
+      int s = cc.j[a] + d[a];
       if (s < 0) {
         const int b = tp.bc[2 * a];
         if (b == 0) s += Ma;
@@ -91,10 +92,18 @@ __device__ __forceinline__ double gather_fstar(const double* __restrict__ F, con
     }
   }
   if (gface >= 0) {
-    if (tp.bc[gface] == 3) return tp.halo[gface & 1][hplane * n + k];
-    return tp.ghost[gface][k];
+    if (tp.bc[gface] == 3) return tp.halo[gface & 1] + hplane * n;
+    return tp.ghost[gface];
   }
-  return F[src * n + k];
+  return F + src * n;
+}
+
+__device__ __forceinline__ double gather_fstar(const double* __restrict__ F, const TransportParams& tp,
+                                               const CellCoord& cc, int k, int kx, int ky, int kz, int n,
+                                               const int8_t (*delta)[kMaxN]) {
+  if (tp.dx == 0) return F[cc.cell * n + k];
+  const int d[3] = {delta[0][kx], tp.dx > 1 ? delta[1][ky] : 0, tp.dx > 2 ? delta[2][kz] : 0};
+  return source_base(F, tp, cc, d, n)[k];
 }
 
 // Copy the shift table into shared memory (call with all threads, then __syncthreads()).

@@ -5,7 +5,7 @@
 
 namespace fks {
 
-// One CTA row per cell slice: grid (chunks, cells); each thread moves 2 consecutive velocities.
+// General transport (any shift size): one CTA row per cell slice, one element per thread.
 __global__ void k_transport(const double* __restrict__ f_in, double* __restrict__ f_out, const TransportParams tp,
                             const uint8_t* __restrict__ solid, int64_t ncells, int n, int N, int dv) {
   __shared__ int8_t sdelta[3][kMaxN];
@@ -22,9 +22,51 @@ __global__ void k_transport(const double* __restrict__ f_in, double* __restrict_
   }
 }
 
+// Transport at CFL <= 1 (every shift in {-1, 0, 1}): per cell the 3^dx possible sources are
+// resolved once (source_base: neighbour cell, ghost vector or halo plane) and every element is a
+// table lookup + one load; persistent CTAs walk the cells.  HBM-bound: 16 B per update.
+template <int N, int DV>
+__global__ void __launch_bounds__(256) k_transport_cfl1(const double* __restrict__ f_in, double* __restrict__ f_out,
+                                                        const TransportParams tp, const uint8_t* __restrict__ solid,
+                                                        int64_t ncells) {
+  constexpr int n = DV == 3 ? N * N * N : N * N;
+  __shared__ int8_t sdelta[3][kMaxN];
+  __shared__ const double* sbase[27];
+  load_delta(tp, sdelta);
+  for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+    __syncthreads();  // sdelta loaded / the previous cell's sources no longer read
+    if (threadIdx.x < 27) {
+      const int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1, (int)threadIdx.x / 9 - 1};
+      const bool is_solid = solid != nullptr && solid[cell];
+      sbase[threadIdx.x] = is_solid ? f_in + cell * n : source_base(f_in, tp, cell_coord(tp, cell), d, n);
+    }
+    __syncthreads();
+    double* out = f_out + cell * n;
+#pragma unroll 8
+    for (int k = threadIdx.x; k < n; k += 256) {
+      const int kx = k % N, ky = (k / N) % N, kz = DV == 3 ? k / (N * N) : 0;
+      const int combo = (sdelta[0][kx] + 1) + 3 * (sdelta[1][ky] + 1) + 9 * (sdelta[2][kz] + 1);
+      out[k] = __ldg(sbase[combo] + k);
+    }
+  }
+}
+
 cudaError_t launch_transport(const double* f_in, double* f_out, const TransportParams& tp, const uint8_t* solid,
                              int64_t ncells, int n, int N, int dv, cudaStream_t s) {
   if (ncells == 0) return cudaSuccess;
+  bool cfl1 = true;  // rows a >= dx are zero
+  for (int a = 0; a < 3; ++a)
+    for (int k = 0; k < N; ++k) cfl1 &= tp.delta[a][k] >= -1 && tp.delta[a][k] <= 1;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned nb = (unsigned)(ncells < (int64_t)sms * 8 ? ncells : (int64_t)sms * 8);
+  if (cfl1) {
+#define FKS_TR(NN, DD) \
+  if (N == NN && dv == DD) { k_transport_cfl1<NN, DD><<<nb, 256, 0, s>>>(f_in, f_out, tp, solid, ncells); return cudaGetLastError(); }
+    FKS_TR(8, 2) FKS_TR(16, 2) FKS_TR(32, 2) FKS_TR(8, 3) FKS_TR(16, 3) FKS_TR(32, 3)
+#undef FKS_TR
+  }
   const int threads = 256;
   const int chunks = (n + threads - 1) / threads;
   dim3 grid(chunks > 64 ? 64 : chunks, (unsigned)(ncells > 65535 ? 65535 : ncells));
