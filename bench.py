@@ -307,6 +307,14 @@ def main():
                                        "hbm_gbs": gbs, "hbm_peak_gbs": peak,
                                        "hbm_frac": gbs / peak if peak else None,
                                        "what": "fks_transport (a1+a3, 16 B per phase-space update), HBM-bound"}
+        rho = torch.empty(ncells, dtype=torch.float64, device=fa.device)
+        uu = torch.empty(ncells, dv, dtype=torch.float64, device=fa.device)
+        TT = torch.empty(ncells, dtype=torch.float64, device=fa.device)
+        ms_m = timed(lambda: ctx.moments(fa, rho, uu, TT), reps)
+        gbs = ncells * n * 8 / (ms_m * 1e-3) / 1e9
+        extra["moments_only"] = {"value": ncells / (ms_m * 1e-3), "unit": "cells/s", "ms": ms_m, "hbm_gbs": gbs,
+                                 "hbm_frac": gbs / hbm_peak(),
+                                 "what": "fks_moments (a10, 8 B read per phase-space point), HBM-bound"}
         ctx.check()
 
     # ---- e2e through the C ABI with host buffers (H2D + step + D2H per step) --------------

@@ -88,49 +88,115 @@ cudaError_t launch_copy_cells(const double* f_in, double* f_out, const int* cell
   return cudaGetLastError();
 }
 
-// a10: one CTA per cell, fixed-order tree reduction (deterministic).
-__global__ void k_moments(const double* __restrict__ f, double* rho, double* u, double* T, int N, int dv, double L,
-                          double h) {
-  __shared__ double red[5][256];
-  const int64_t cell = blockIdx.x;
-  const int n = dv == 3 ? N * N * N : N * N;
-  double m[5] = {0, 0, 0, 0, 0};
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const double fk = f[cell * n + k];
-    const double vx = node_v(k % N, L, h), vy = node_v((k / N) % N, L, h);
-    const double vz = dv == 3 ? node_v(k / (N * N), L, h) : 0.0;
-    m[0] += fk;
-    m[1] += vx * fk;
-    m[2] += vy * fk;
-    m[3] += vz * fk;
-    m[4] += (vx * vx + vy * vy + vz * vz) * fk;
-  }
-  for (int c = 0; c < 5; ++c) red[c][threadIdx.x] = m[c];
-  __syncthreads();
-  for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
-    if ((int)threadIdx.x < w)
-      for (int c = 0; c < 5; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + w];
+// a10: one CTA per cell (persistent), 16-byte loads, fixed-order reduction (warp
+// shuffles, then warps in order): deterministic.  HBM-bound: 8 B read per phase-space point.
+template <int N, int DV>
+__global__ void __launch_bounds__(256) k_moments(const double* __restrict__ f, double* rho, double* u, double* T,
+                                                 int64_t ncells, double L, double h) {
+  constexpr int n = DV == 3 ? N * N * N : N * N;
+  __shared__ double red[8][5];
+  for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+    double m[5] = {0, 0, 0, 0, 0};
+    const double2* fc = reinterpret_cast<const double2*>(f + cell * n);
+#pragma unroll 4
+    for (int k2 = threadIdx.x; k2 < n / 2; k2 += 256) {
+      const double2 p = __ldg(fc + k2);
+      const int k = 2 * k2;  // k and k + 1 share v_y, v_z (N even)
+      const double vx0 = node_v(k % N, L, h), vx1 = node_v(k % N + 1, L, h), vy = node_v((k / N) % N, L, h);
+      const double vz = DV == 3 ? node_v(k / (N * N), L, h) : 0.0;
+      const double s = p.x + p.y;
+      m[0] += s;
+      m[1] += vx0 * p.x + vx1 * p.y;
+      m[2] += vy * s;
+      m[3] += vz * s;
+      m[4] += (vx0 * vx0 + vy * vy + vz * vz) * p.x + (vx1 * vx1 + vy * vy + vz * vz) * p.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
+    }
+    __syncthreads();  // red free (previous cell)
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) red[threadIdx.x >> 5][c] = m[c];
+    }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      double r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+      for (int w = 0; w < 8; ++w) {
+        r0 += red[w][0]; r1 += red[w][1]; r2 += red[w][2]; r3 += red[w][3]; r4 += red[w][4];
+      }
+      double cell_vol = 1.0;
+      for (int a = 0; a < DV; ++a) cell_vol *= h;
+      const double r = cell_vol * r0;
+      const double ux = cell_vol * r1 / r, uy = cell_vol * r2 / r, uz = cell_vol * r3 / r;
+      const double e = cell_vol * r4 / r;
+      rho[cell] = r;
+      u[cell * DV + 0] = ux;
+      u[cell * DV + 1] = uy;
+      if (DV == 3) u[cell * DV + 2] = uz;
+      T[cell] = (e - (ux * ux + uy * uy + uz * uz)) / DV;
+    }
   }
-  if (threadIdx.x == 0) {
-    double cell_vol = 1.0;
-    for (int a = 0; a < dv; ++a) cell_vol *= h;
-    const double r = cell_vol * red[0][0];
-    const double ux = cell_vol * red[1][0] / r, uy = cell_vol * red[2][0] / r, uz = cell_vol * red[3][0] / r;
-    const double e = cell_vol * red[4][0] / r;
-    rho[cell] = r;
-    u[cell * dv + 0] = ux;
-    u[cell * dv + 1] = uy;
-    if (dv == 3) u[cell * dv + 2] = uz;
-    T[cell] = (e - (ux * ux + uy * uy + uz * uz)) / dv;
+}
+
+// Small cells (2D): one warp per cell, same arithmetic order per lane, shuffle reduction.
+template <int N>
+__global__ void __launch_bounds__(256) k_moments_warp(const double* __restrict__ f, double* rho, double* u, double* T,
+                                                      int64_t ncells, double L, double h) {
+  constexpr int n = N * N;
+  const int lane = threadIdx.x & 31;
+  for (int64_t cell = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); cell < ncells; cell += (int64_t)gridDim.x * 8) {
+    double m[4] = {0, 0, 0, 0};
+    const double2* fc = reinterpret_cast<const double2*>(f + cell * n);
+#pragma unroll 4
+    for (int k2 = lane; k2 < n / 2; k2 += 32) {
+      const double2 p = __ldg(fc + k2);
+      const int k = 2 * k2;
+      const double vx0 = node_v(k % N, L, h), vx1 = node_v(k % N + 1, L, h), vy = node_v(k / N, L, h);
+      const double s = p.x + p.y;
+      m[0] += s;
+      m[1] += vx0 * p.x + vx1 * p.y;
+      m[2] += vy * s;
+      m[3] += (vx0 * vx0 + vy * vy) * p.x + (vx1 * vx1 + vy * vy) * p.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
+    }
+    if (lane == 0) {
+      const double cell_vol = h * h;
+      const double r = cell_vol * m[0];
+      const double ux = cell_vol * m[1] / r, uy = cell_vol * m[2] / r;
+      const double e = cell_vol * m[3] / r;
+      rho[cell] = r;
+      u[cell * 2 + 0] = ux;
+      u[cell * 2 + 1] = uy;
+      T[cell] = (e - (ux * ux + uy * uy)) / 2;
+    }
   }
 }
 
 cudaError_t launch_moments(const double* f, double* rho, double* u, double* T, int64_t ncells, int N, int dv,
                            double L, double h, cudaStream_t s) {
   if (ncells == 0) return cudaSuccess;
-  k_moments<<<(unsigned)ncells, 256, 0, s>>>(f, rho, u, T, N, dv, L, h);
-  return cudaGetLastError();
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned nb = (unsigned)(ncells < (int64_t)sms * 8 ? ncells : (int64_t)sms * 8);
+  if (dv == 2) {
+    const unsigned nw = (unsigned)((ncells + 7) / 8 < (int64_t)sms * 8 ? (ncells + 7) / 8 : (int64_t)sms * 8);
+    if (N == 8) { k_moments_warp<8><<<nw, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
+    if (N == 16) { k_moments_warp<16><<<nw, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
+    if (N == 32) { k_moments_warp<32><<<nw, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
+  }
+#define FKS_MO(NN, DD) \
+  if (N == NN && dv == DD) { k_moments<NN, DD><<<nb, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
+  FKS_MO(8, 2) FKS_MO(16, 2) FKS_MO(32, 2) FKS_MO(8, 3) FKS_MO(16, 3) FKS_MO(32, 3)
+#undef FKS_MO
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace fks
