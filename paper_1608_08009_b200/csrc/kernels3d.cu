@@ -68,14 +68,22 @@ struct Cfg3 {
   static constexpr size_t TBUF_BYTES = ((size_t)SLAB * 16 + 127) / 128 * 128;
   static constexpr size_t OFF_TBUF = 0;                       // two table slabs (double-buffered)
   static constexpr size_t OFF_PLN = OFF_TBUF + 2 * TBUF_BYTES;  // two plane slabs
-  // mbarriers: tbar[2], wbar[2], fsb[2] (f* cache written), fse[2] (f* cache read)
+  // Per-warp pipelines: warp w of a group handles the planes tl in [w WPL, (w+1) WPL); the
+  // table slab is loaded per table group (TGW warps that share mirror-pair rows).
+  static constexpr int NW = GT / 32;                   // warps per group
+  static constexpr int WPL = NP / NW;                  // planes per warp
+  static constexpr int TGW = NW >= 2 ? 2 : 1;          // warps per table group
+  static constexpr int NTG = NW / TGW;                 // table groups
+  // mbarriers: tbar[2][NTG], wbar[2][NW], fsb[2] (f* cache written), fse[2] (f* cache read)
+  static constexpr int NMBAR = 2 * NTG + 2 * NW + 4;
   static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;
-  static constexpr size_t OFF_TMEM = OFF_MBAR + 64;
+  static constexpr size_t OFF_TMEM = OFF_MBAR + 8 * NMBAR;
   static constexpr size_t OFF_PART = OFF_TMEM + 8;           // lambda[5] + warp partials [4][5]
   static constexpr size_t OFF_DELTA = OFF_PART + 32 * 8;  // int8 [3][kMaxN] shift table
   static constexpr size_t SMEM = OFF_DELTA + 3 * kMaxN;
   static_assert(GT % 32 == 0, "warp groups must be whole warps");
   static_assert(NP % 2 == 0, "mirror pairs stay within a CTA");
+  static_assert(NP % NW == 0 && (NW == 1 || WPL == 1), "whole planes per warp");
   static_assert(2 * ((SLAB * 16 + 127) / 128 * 128) >= (size_t)NP * N * N * 16,
                 "the two table buffers hold one plane slab (z-group forward)");
   static_assert(GT <= 128, "one TMEM lane per z-group thread");
@@ -216,10 +224,10 @@ __device__ __forceinline__ void zpass_store(const double2 (&x)[N], double2* Wb, 
 // Group synchronisation through L2 (the P CTAs of a cell group are co-resident: cooperative
 // launch, one CTA per SM).  Every exchange buffer use is an item of a per-group sequence
 // (per cell: the forward xy transform, then z(0) .. z(D-1)); item s lives in ring slot s % NBUF.
-// Each of the P producers adds 1 to prod[slot] after writing its part (release), each of the P
-// consumers adds 1 to cons[slot] once its read has completed; a producer of item s first waits
-// for cons[slot] >= P * (s / NBUF), a consumer for prod[slot] >= P * (s / NBUF + 1).  The
-// counters are zeroed before every launch.
+// Counts are in warps: each of the NW * P producing warps adds 1 to prod[slot] after writing its
+// part (release), each of the NW * P consuming warps adds 1 to cons[slot] once its read has
+// completed; a producer of item s first waits for cons[slot] >= NW P (s / NBUF), a consumer for
+// prod[slot] >= NW P (s / NBUF + 1).  The counters are zeroed before every launch.
 struct GroupSync {
   static constexpr int NB = 4;  // = Cfg3::NBUF
   unsigned prod[NB];
@@ -231,6 +239,14 @@ struct GroupSync {
 
 __device__ __forceinline__ void sync_signal(unsigned* ctr) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+}
+
+__device__ __forceinline__ void sync_signal_n(unsigned* ctr, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(ctr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void sync_signal_relaxed_n(unsigned* ctr, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;\n" ::"l"(ctr), "r"(v) : "memory");
 }
 
 // Consumer-side signal: the reads it announces have completed (their data is in registers or
@@ -276,8 +292,8 @@ struct Ctx3 {
   using C = Cfg3<N, P>;
   double2* tbuf;   // 2 x table slab [SLABR rows][N l_x] (direction g in buffer g & 1)
   double2* pln0;   // 2 x [NP j_z][N y][N x] plane slabs (swizzled)
-  uint64_t* tbar;  // [2] table slab landed
-  uint64_t* wbar;  // [2] plane slab landed
+  uint64_t* tbar;  // [2][NTG] table rows of a table group landed
+  uint64_t* wbar;  // [2][NW] plane(s) of a warp landed
   uint64_t* fsb;   // [2] f* cache of parity b written (z group, GT arrivals)
   uint64_t* fse;   // [2] f* cache of parity b read for the last time (xy group, GT arrivals)
   double* part;    // [8] epilogue scratch (moment sums, lambda)
@@ -303,18 +319,29 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
   GroupSync* gs = c.gs;
   const int ly = plane_of<N>(rank * NP + tl);  // this thread's pencil (l_x = tx, l_y)
   const TabMap tm = tab_map<N, NP>(rank, tl);
-  // rows of this CTA's table slab (the last entry's extent)
-  const uint32_t kTabBytes = [&] {
-    const TabMap last = tab_map<N, NP>(rank, NP - 1);
-    const int rows = last.mode == 1 ? last.base + N : last.mode == 2 ? last.base + N / 2 + 1 : last.base + N;
-    return (uint32_t)rows * N * 16;
-  }();
+  constexpr int NW = C::NW, NTG = C::NTG, TGW = C::TGW;
+  constexpr unsigned WP = NW * P;  // signals per exchange item
+  const int w = tg >> 5, lane = tg & 31;
+  // table group of this warp and its rows of the CTA's table slab: [trow0, trow1)
+  const int tgi = w / TGW;
+  const bool tg_leader = (w % TGW) == 0 && lane == 0;
+  auto rows_end = [&](int tl_last) {
+    const TabMap m = tab_map<N, NP>(rank, tl_last);
+    return m.mode == 1 ? m.base + N : m.mode == 2 ? m.base + N / 2 + 1 : m.base + N;
+  };
+  const int trow0 = tab_map<N, NP>(rank, tgi * TGW * C::WPL).base;
+  const int trow1 = rows_end((tgi + 1) * TGW * C::WPL - 1);
   const double2* tab_rank = p.tables + (size_t)rank * C::SLAB;  // + direction * P * SLAB
   constexpr size_t TB = C::TBUF_BYTES / 16;  // complex elements per table buffer
-  auto load_tab = [&](int j) {  // thread 0: direction j -> table buffer j & 1
-    bulk_load(c.tbuf + (j & 1) * TB, tab_rank + (size_t)j * P * C::SLAB, kTabBytes, c.tbar + (j & 1));
+  auto load_tab = [&](int j) {  // tg_leader: this group's rows of direction j -> table buffer j & 1
+    bulk_load(c.tbuf + (j & 1) * TB + (size_t)trow0 * N, tab_rank + (size_t)j * P * C::SLAB + (size_t)trow0 * N,
+              (uint32_t)(trow1 - trow0) * N * 16, c.tbar + (j & 1) * NTG + tgi);
   };
-  uint32_t tphase = 0;  // bit b: parity of table buffer b
+  auto group_sync = [&]() {  // the warps of this table group
+    if constexpr (TGW == 2) named_bar(3 + tgi, 64);
+    else __syncwarp();
+  };
+  uint32_t tphase = 0;  // bit b: parity of this group's table buffer b
   unsigned seq = 0;     // exchange-buffer sequence index of the next item
   unsigned ncell = 0;   // cells done by this group
   for (int it = cid; it < p.ncells; it += c.ncl, ++ncell) {
@@ -393,9 +420,9 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
         for (int y = 0; y < N; ++y) cc[y] = col[y * N + swz(y, tx)];
         fft<N, -1>(cc);
         // the slot's previous item must have been read by every consumer
-        if (tg == 0 && s_fwd / NB > 0) sync_wait_free(&gs->cons[s_fwd % NB], P * (s_fwd / NB), 0u);
+        if (tg == 0 && s_fwd / NB > 0) sync_wait_free(&gs->cons[s_fwd % NB], WP * (s_fwd / NB), 0u);
         named_bar(1, GT);  // also: every plane read, the table buffers may be refilled
-        if (tg == 0) {
+        if (tg_leader) {
           load_tab(0);
           if (D > 1) load_tab(1);
         }
@@ -404,12 +431,12 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
         for (int l = 0; l < N; ++l) Wb[l * N + swz(l, tx)] = cc[l];
       }
       named_bar(1, GT);
-      if (tg == 0) sync_signal(&gs->prod[s_fwd % NB]);
+      if (tg == 0) sync_signal_n(&gs->prod[s_fwd % NB], NW);
       TSTAMPB(2);
     }
     {  // z transform of the forward item of every CTA -> f^ pencil in TMEM
       const unsigned slot = s_fwd % NB, use = s_fwd / NB;
-      if (tg == 0) sync_wait(&gs->prod[slot], P * (use + 1));
+      if (tg == 0) sync_wait(&gs->prod[slot], WP * (use + 1));
       TSTAMPB(9);
       named_bar(1, GT);
       double2 x[N];
@@ -432,7 +459,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       tmem_wait_st();
       named_bar(1, GT);  // every column of the forward item read
       TSTAMPB(10);
-      if (tg == 0) sync_signal_relaxed(&gs->cons[slot]);
+      if (tg == 0) sync_signal_relaxed_n(&gs->cons[slot], NW);
       seq = s_fwd + 1;
     }
 #pragma unroll 1
@@ -441,26 +468,28 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       const unsigned slot = seq % NB, use = seq / NB;
       double2 x[N];
       // slot free once its previous item has been read by every consumer (polled early)
-      const unsigned cons_seen = tg == 0 && use > 0 ? ld_relaxed(&gs->cons[slot]) : 0u;
+      const unsigned cons_seen = lane == 0 && use > 0 ? ld_relaxed(&gs->cons[slot]) : 0u;
       const int tb = j & 1;
-      mbar_wait(c.tbar + tb, (tphase >> tb) & 1u);
+      mbar_wait(c.tbar + tb * NTG + tgi, (tphase >> tb) & 1u);
       tphase ^= 1u << tb;
       TSTAMP(2048 + j * 8 + 1);
       zpass_compute<N, P>(taddr, c.tbuf + tb * TB, tx, tm, x);
       TSTAMP(2048 + j * 8 + 2);
-      if (tg == 0 && use > 0) sync_wait_free(&gs->cons[slot], P * use, cons_seen);
-      named_bar(1, GT);  // table buffer tb consumed; the z(j-1) stores of every thread precede this point
-      if (tg == 0) {
-        if (j + 2 < D) load_tab(j + 2);  // into the buffer just freed
-        // publish z(j-1): its stores had a whole z pass to drain, so the release is cheap
+      group_sync();  // this group's table buffer tb consumed; the warp's z(j-1) stores precede this
+      if (tg_leader && j + 2 < D) load_tab(j + 2);  // into the buffer just freed
+      if (lane == 0) {
+        if (use > 0) sync_wait_free(&gs->cons[slot], WP * use, cons_seen);
+        // publish this warp's z(j-1): its stores had a whole z pass to drain (cheap release)
         if (j > 0) sync_signal(&gs->prod[(seq - 1) % NB]);
       }
+      __syncwarp();
       zpass_store<N, P>(x, c.W + slot * C::WBUF, ly, tx);
       TSTAMP(2048 + j * 8 + 3);
       ++seq;
     }
-    named_bar(1, GT);  // the z(D-1) stores of every thread precede the release; tables consumed
-    if (tg == 0) sync_signal(&gs->prod[(seq - 1) % NB]);
+    __syncwarp();  // this warp's z(D-1) stores precede the release
+    if (lane == 0) sync_signal(&gs->prod[(seq - 1) % NB]);
+    named_bar(1, GT);  // every warp done with the tables before the next forward reuses them
   }
 }
 
@@ -477,16 +506,21 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
   uint32_t wphase = 0;  // bit b = parity of plane buffer b
   unsigned seq = 0;     // exchange-buffer sequence index of the next item
   unsigned ncell = 0;   // cells done by this group
-  // thread 0: W(item s) -> plane buffer b, once every producer has published it (`seen`: an
-  // earlier relaxed read of the counter)
+  constexpr int NW = C::NW, WPL = C::WPL;
+  constexpr unsigned WP = NW * P;  // signals per exchange item
+  const int w = tg >> 5, lane = tg & 31;
+  // lane 0 of each warp: its planes of W(item s) -> plane buffer b, once every producer has
+  // published the item (`seen`: an earlier relaxed read of the counter)
   auto issue_load = [&](unsigned s, int b, unsigned seen) {
     const unsigned* ctr = &gs->prod[s % NB];
-    const unsigned target = P * (s / NB + 1);
+    const unsigned target = WP * (s / NB + 1);
     // The producers' release put their stores in L2 before the counter moved, and the bulk copy
     // reads L2 after the (control-dependent) check, so a relaxed observation is enough here.
     if ((int)(seen - target) < 0) sync_wait(ctr, target);
     asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic-proxy stores -> bulk reads
-    bulk_load(c.pln0 + b * C::PSLAB, c.W + (s % NB) * C::WBUF + (size_t)rank * C::PSLAB, kPlaneBytes, c.wbar + b);
+    bulk_load(c.pln0 + b * C::PSLAB + (size_t)w * WPL * N * N,
+              c.W + (s % NB) * C::WBUF + (size_t)(rank * NP + w * WPL) * N * N, kPlaneBytes / NW,
+              c.wbar + b * NW + w);
   };
   for (int it = cid; it < p.ncells; it += c.ncl, ++ncell) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
@@ -516,7 +550,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
     };
     seq += 1;  // the forward item (z group's)
     TSTAMPB(3);
-    if (tg == 0) issue_load(seq, 0, 0u);  // z(0): both plane buffers are free here
+    if (lane == 0) issue_load(seq, 0, 0u);  // z(0): both plane buffers are free here
     double q[N];  // gain accumulator of column (tx, tl), then Q
 #pragma unroll
     for (int y = 0; y < N; ++y) q[y] = 0.0;
@@ -525,11 +559,11 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
       TSTAMP(d * 8);
       const int pb = d & 1;
       double2* pln = c.pln0 + pb * C::PSLAB;
-      mbar_wait(c.wbar + pb, (wphase >> pb) & 1u);
+      mbar_wait(c.wbar + pb * NW + w, (wphase >> pb) & 1u);
       wphase ^= 1u << pb;
       unsigned prod_seen = 0;
-      if (tg == 0) {
-        sync_signal_relaxed(&gs->cons[seq % NB]);  // W(d) read by this CTA
+      if (lane == 0) {
+        sync_signal_relaxed(&gs->cons[seq % NB]);  // this warp's planes of W(d) read
         if (d + 1 < D) prod_seen = ld_relaxed(&gs->prod[(seq + 1) % NB]);  // checked after pass 0
       }
       TSTAMP(d * 8 + 1);
@@ -546,8 +580,8 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         if (pass == 0) {
 #pragma unroll
           for (int x = 0; x < N; ++x) pl[at(x)] = cc[x];
-          named_bar(2, GT);  // rows done; every thread has also finished xy(d-1): buffer pb^1 free
-          if (tg == 0 && d + 1 < D) issue_load(seq + 1, pb ^ 1, prod_seen);
+          __syncwarp();  // rows done; this warp has also finished xy(d-1): its buffer pb^1 is free
+          if (lane == 0 && d + 1 < D) issue_load(seq + 1, pb ^ 1, prod_seen);
           TSTAMP(d * 8 + 2);
         } else if (d < p.A) {
 #pragma unroll
@@ -674,9 +708,9 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.tbuf = reinterpret_cast<double2*>(smem + C::OFF_TBUF);
   c.pln0 = reinterpret_cast<double2*>(smem + C::OFF_PLN);
   c.tbar = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR);
-  c.wbar = c.tbar + 2;
-  c.fsb = c.tbar + 4;
-  c.fse = c.tbar + 6;
+  c.wbar = c.tbar + 2 * C::NTG;
+  c.fsb = c.wbar + 2 * C::NW;
+  c.fse = c.fsb + 2;
   c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
   int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::OFF_DELTA);
   load_delta(p.tp, sdelta);
@@ -699,10 +733,8 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   if (t == 0) {
-    mbar_init(c.tbar, 1);
-    mbar_init(c.tbar + 1, 1);
-    mbar_init(c.wbar, 1);
-    mbar_init(c.wbar + 1, 1);
+    for (int i = 0; i < 2 * C::NTG; ++i) mbar_init(c.tbar + i, 1);
+    for (int i = 0; i < 2 * C::NW; ++i) mbar_init(c.wbar + i, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(c.fsb + i, C::GT);
       mbar_init(c.fse + i, C::GT);
