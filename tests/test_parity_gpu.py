@@ -213,6 +213,47 @@ def test_transport_bitwise(torch, fks, dxd, dv, M, N, bc):
     np.testing.assert_array_equal(host(a), ref)
 
 
+@pytest.mark.parametrize("cfl", [1.7, 2.6])
+def test_transport_bitwise_cfl_above_one(torch, fks, cfl):
+    """Shifts of 2-3 cells per step (CFL > 1) take the general gather kernel: still bitwise."""
+    dxd, dv, M, N, L = 2, 3, [6, 5], 8, 5.0
+    bc = [transport.PERIODIC, transport.PERIODIC, transport.GHOST, transport.OUTFLOW]
+    F, h, _, ghosts = _spatial_case(dxd, dv, M, N, L, bc, seed=11)
+    dt = cfl * h / (L - L / N)
+    assert np.max(np.abs(transport.shift_delta(0, N, L, dt, h))) >= 2
+    ctx = fks.Context(dv, dxd, M, N, L, 24, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(4):
+        ctx.transport(a, b, dt)
+        a, b = b, a
+        ref = transport.gather(ref, s, dxd, dv, N, L, dt, h, bc, ghosts)
+    np.testing.assert_array_equal(host(a), ref)
+
+
+@pytest.mark.parametrize("N,L,ncells", [(16, 6.0, 23), (32, 9.0, 9)])
+def test_collide_3d_one_group_many_cells(torch, fks, N, L, ncells, monkeypatch):
+    """One CTA group walks every cell: the exchange ring wraps many times, the f* cache parity and
+    the next-cell forward overlap are exercised on every cell boundary."""
+    monkeypatch.setenv("FKS_MAX_CLUSTERS", "1")
+    f = workloads.family("random", 3, N, L, ncells, seed=21)
+    ctx = fks.Context(3, 0, [ncells], N, L, 24)
+    Q = torch.empty(ncells, N, N, N, dtype=torch.float64, device="cuda")
+    ctx.collide(dev(torch, f), Q)
+    tab = tables.build_tables(3, N, L)
+    assert rel_err_Q(host(Q), f, tab, direct=False) <= TOL
+    # and the fused step on the same single group (projection reduction, Euler, TMEM f* cache)
+    c = workloads.config("C2")
+    g = torch.empty_like(Q)
+    ctx.step(dev(torch, f), g, c["dt"])
+    ref = ostep.homogeneous_step(f, tab, c["dt"])
+    got = host(g)
+    for i in range(ncells):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
 # ---------------------------------------------------------------- a10, flags, determinism, e2e
 def test_moments(torch, fks):
     for dv, N, L in [(2, 32, 9.0), (3, 16, 7.0)]:
