@@ -56,7 +56,10 @@ struct Cfg3 {
   static constexpr int PSLAB = NP * N * N;    // complex elements of a plane slab
   static constexpr int WPLANE = N * N;        // plane in the exchange buffer
   static constexpr size_t WBUF = (size_t)N * WPLANE;  // one exchange buffer (all N j_z planes)
-  static constexpr int NBUF = 4;  // z stores z(k+1) while phase k is still completing
+#ifndef FKS_NBUF
+#define FKS_NBUF 4
+#endif
+  static constexpr int NBUF = FKS_NBUF;  // exchange ring slots: the z group runs up to NBUF-1 items ahead
   static constexpr int FHAT_COLS = 4 * N;     // one f^ pencil (N complex fp64) per lane (z group)
   // f* column cache (xy group, N >= 16): column (l_x = tx, j_z) of f* (N fp64 = 2N columns),
   // read back by the loss term and the Euler update instead of re-gathering f from HBM.
@@ -229,7 +232,7 @@ __device__ __forceinline__ void zpass_store(const double2 (&x)[N], double2* Wb, 
 // completed; a producer of item s first waits for cons[slot] >= NW P (s / NBUF), a consumer for
 // prod[slot] >= NW P (s / NBUF + 1).  The counters are zeroed before every launch.
 struct GroupSync {
-  static constexpr int NB = 4;  // = Cfg3::NBUF
+  static constexpr int NB = FKS_NBUF;  // = Cfg3::NBUF
   unsigned prod[NB];
   unsigned cons[NB];
   unsigned part;                // projection partial sums published (cumulative, P per cell)
@@ -361,7 +364,10 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
     {  // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[s_fwd % NB]
       double2* pln = c.tbuf;  // both table buffers: one plane slab
       constexpr int PER = NP * N * N / GT;  // = N elements per thread
-      constexpr int B = PER < 16 ? PER : 16;
+#ifndef FKS_GATHER_B
+#define FKS_GATHER_B 32  // f* loads in flight per thread in the forward gather (one L2 round trip)
+#endif
+      constexpr int B = PER < FKS_GATHER_B ? PER : FKS_GATHER_B;
 #pragma unroll 1
       for (int b0 = 0; b0 < PER; b0 += B) {
         double v[B];
