@@ -12,6 +12,7 @@ struct TransportParams {
   int dx;                  // space dimension 0..3
   int M[3];                // local cells per space axis (axis 0 fastest)
   int bc[6];               // FKS_BC_* per face
+  int cfl1;                // every |delta| <= 1 (the 3^dx-sources fast paths apply)
   int8_t delta[3][kMaxN];  // delta[a][k_a] = s^{n+1} - s^n for velocity component a
   const double* ghost[6];  // ghost vectors (n values) of GHOST faces, device memory
   const double* halo[2];   // HALO faces of the slowest axis: neighbour rank's boundary plane

@@ -327,6 +327,9 @@ void fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift)
   tp->halo[1] = c->halo[1];
   if (with_shift)
     for (int a = 0; a < c->grid.dx; ++a) shift_delta(c->step_n, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
+  tp->cfl1 = 1;
+  for (int a = 0; a < 3; ++a)
+    for (int k = 0; k < fks::kMaxN; ++k) tp->cfl1 &= tp->delta[a][k] >= -1 && tp->delta[a][k] <= 1;
 }
 
 fks::StepParams base_params(fks_ctx* c, const double* f_in, double* f_out, int mode) {

@@ -149,8 +149,19 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
     {
       double2 r[N];
 #pragma unroll
-      for (int x = 0; x < N; ++x)
-        r[x] = make_double2(gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta), 0.0);
+      for (int x = 0; x < N; ++x) r[x].y = 0.0;
+      if (p.tp.dx == 0) {  // the row is contiguous: 16-byte loads, all in flight at once
+        const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * (int64_t)n + N * tx);
+#pragma unroll
+        for (int x = 0; x < N / 2; ++x) {
+          const double2 v = __ldg(src + x);
+          r[2 * x].x = v.x;
+          r[2 * x + 1].x = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < N; ++x) r[x].x = gather_fstar(p.f_in, p.tp, cc, x + N * tx, x, tx, 0, n, sdelta);
+      }
       if constexpr (C::FS_TMEM) {
 #pragma unroll
         for (int ch = 0; ch < N / 16; ++ch) {

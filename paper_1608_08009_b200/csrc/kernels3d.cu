@@ -82,7 +82,8 @@ struct Cfg3 {
   static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;
   static constexpr size_t OFF_TMEM = OFF_MBAR + 8 * NMBAR;
   static constexpr size_t OFF_PART = OFF_TMEM + 8;           // lambda[5] + warp partials [4][5]
-  static constexpr size_t OFF_DELTA = OFF_PART + 32 * 8;  // int8 [3][kMaxN] shift table
+  static constexpr size_t OFF_SBASE = OFF_PART + 32 * 8;  // [27] transport sources of the cell
+  static constexpr size_t OFF_DELTA = OFF_SBASE + 27 * 8;  // int8 [3][kMaxN] shift table
   static constexpr size_t SMEM = OFF_DELTA + 3 * kMaxN;
   static_assert(GT % 32 == 0, "warp groups must be whole warps");
   static_assert(NP % 2 == 0, "mirror pairs stay within a CTA");
@@ -301,6 +302,7 @@ struct Ctx3 {
   uint64_t* fse;   // [2] f* cache of parity b read for the last time (xy group, GT arrivals)
   double* part;    // [8] epilogue scratch (moment sums, lambda)
   const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
+  const double** sbase;          // [27] per-cell transport sources (forward gather, dx > 0)
   double2* W;      // [NBUF][N j_z][N l_y][N l_x] exchange buffers of this group (L2, swizzled)
   GroupSync* gs;   // this group's counters
   int rank, cid, ncl, tg, tx, tl;
@@ -371,11 +373,32 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
 #pragma unroll 1
       for (int b0 = 0; b0 < PER; b0 += B) {
         double v[B];
+        if (p.tp.dx == 0) {  // this CTA's planes are contiguous: every load in flight at once
+          const double* src = p.f_in + cell * (int64_t)n + (int64_t)rank * NP * N * N;
 #pragma unroll
-        for (int j = 0; j < B; ++j) {
-          const int e = tg + (b0 + j) * GT;
-          const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
-          v[j] = gather_fstar(p.f_in, p.tp, cc_cell, x + N * (y + N * zz), x, y, zz, n, c.delta);
+          for (int j = 0; j < B; ++j) v[j] = __ldg(src + tg + (b0 + j) * GT);
+        } else if (p.tp.cfl1) {  // sources per shift combination resolved once per cell, then lookups
+          if (b0 == 0) {
+            if (tg < 27) {
+              const int d[3] = {tg % 3 - 1, (tg / 3) % 3 - 1, tg / 9 - 1};
+              c.sbase[tg] = source_base(p.f_in, p.tp, cc_cell, d, n);
+            }
+            named_bar(1, GT);
+          }
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            const int e = tg + (b0 + j) * GT;
+            const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
+            const int combo = (c.delta[0][x] + 1) + 3 * (c.delta[1][y] + 1) + 9 * (c.delta[2][zz] + 1);
+            v[j] = c.sbase[combo][x + N * (y + N * zz)];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            const int e = tg + (b0 + j) * GT;
+            const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
+            v[j] = gather_fstar(p.f_in, p.tp, cc_cell, x + N * (y + N * zz), x, y, zz, n, c.delta);
+          }
         }
 #pragma unroll
         for (int j = 0; j < B; ++j) {
@@ -718,6 +741,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.fsb = c.wbar + 2 * C::NW;
   c.fse = c.fsb + 2;
   c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
+  c.sbase = reinterpret_cast<const double**>(smem + C::OFF_SBASE);
   int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::OFF_DELTA);
   load_delta(p.tp, sdelta);
   c.delta = sdelta;

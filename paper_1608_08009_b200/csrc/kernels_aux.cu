@@ -54,9 +54,7 @@ __global__ void __launch_bounds__(256) k_transport_cfl1(const double* __restrict
 cudaError_t launch_transport(const double* f_in, double* f_out, const TransportParams& tp, const uint8_t* solid,
                              int64_t ncells, int n, int N, int dv, cudaStream_t s) {
   if (ncells == 0) return cudaSuccess;
-  bool cfl1 = true;  // rows a >= dx are zero
-  for (int a = 0; a < 3; ++a)
-    for (int k = 0; k < N; ++k) cfl1 &= tp.delta[a][k] >= -1 && tp.delta[a][k] <= 1;
+  const bool cfl1 = tp.cfl1 != 0;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
