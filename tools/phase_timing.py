@@ -43,3 +43,13 @@ for c in range(2):
         v = ts[1024 + c * 16 + i]
         if v:
             print(f"  cell{c} {nm:24s} {v - base:8d}")
+# per-rank global timer (ns) of group 0: xy direction tops, epilogue, z stores done
+buf2 = (ctypes.c_longlong * 4096)()
+_lib.load().fks_debug_tstamps(buf2, 4096)
+g = np.array(buf2[:])[3072:3072 + 8 * 128].reshape(8, 128)
+t0 = g[:, 0].min()
+print("rank | xy top d=0,5,10,15,20,24 (cell0, us) | epi start, lambda (cell0) | z stored j=23 cell0 | xy top d=0 cell1")
+for r in range(8):
+    row = g[r]
+    f = lambda v: f"{(v - t0) / 1000:7.2f}" if v else "   -   "
+    print(r, "|", " ".join(f(row[d]) for d in (0, 5, 10, 15, 20, 24)), "|", f(row[30]), f(row[31]), "|", f(row[80 + 23]), "|", f(row[40]))
