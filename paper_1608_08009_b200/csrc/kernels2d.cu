@@ -216,19 +216,25 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
         if (pass == 0) {
 #pragma unroll
           for (int ch = 0; ch < N / 8; ++ch) {
+            // table entries first: their shared-memory latency overlaps the TMEM load's
+            double2 tt[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int ly = ch * 8 + i;
+              if (TAB_SMEM) {
+                const int row = neg ? (N - ly) & (N - 1) : ly;
+                tt[i] = tab[((size_t)d * N + row) * HC + tcol];
+              } else {
+                tt[i] = __ldg(p.tables + (size_t)d * n + ly * N + tx);
+              }
+            }
             uint32_t v[32];
             tmem2_ld32(taddr + ch * 32, v);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int ly = ch * 8 + i;
-              double2 t;
-              if (TAB_SMEM) {
-                const int row = neg ? (N - ly) & (N - 1) : ly;
-                t = tab[((size_t)d * N + row) * HC + tcol];
-              } else {
-                t = __ldg(p.tables + (size_t)d * n + ly * N + tx);
-              }
+              const double2 t = tt[i];
               const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
               const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
               c[ly] = make_double2(fma(t.x, Fx, -t.y * Fy), fma(t.x, Fy, t.y * Fx));

@@ -195,6 +195,14 @@ __device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbu
   const double2* tr = tbuf + tm.base * N + ((N - tx) & (N - 1));  // mirrored column
 #pragma unroll
   for (int ch = 0; ch < N / 8; ++ch) {  // 8 complex fp64 = 32 TMEM columns per chunk
+    double2 tt[8];  // table entries first: their shared-memory latency overlaps the TMEM load's
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int lz = ch * 8 + i;
+      const int lzm = (N - lz) & (N - 1);
+      const bool mir = tm.mode == 1 || (tm.mode == 2 && lz > N / 2);
+      tt[i] = mir ? tr[lzm * N] : td[lz * N];
+    }
     uint32_t v[32];
     tmem_ld32(taddr + ch * 32, v);
     tmem_wait_ld();
@@ -203,9 +211,7 @@ __device__ __forceinline__ void zpass_compute(uint32_t taddr, const double2* tbu
       const int lz = ch * 8 + i;
       const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
       const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
-      const int lzm = (N - lz) & (N - 1);
-      const bool mir = tm.mode == 1 || (tm.mode == 2 && lz > N / 2);
-      const double2 T = mir ? tr[lzm * N] : td[lz * N];
+      const double2 T = tt[i];
       x[lz] = make_double2(fma(T.x, Fx, -T.y * Fy), fma(T.x, Fy, T.y * Fx));
     }
   }
