@@ -299,6 +299,17 @@ def main():
         ms_c = timed(lambda: ctx.collide(fa, fb), reps)
         extra["collide_only"] = {"value": nfluid_local / (ms_c * 1e-3), "unit": "cells/s", "ms": ms_c,
                                  "what": "fks_collide (a4-a7, Q only), same cells"}
+        if dv == 3 and c["dx_dim"] == 0:  # the 8x8 product grid (A = 64) as secondary
+            ctx64 = fks.Context(dv, 0, [ncells], N, c["L"], 64)
+            ctx64.set_params(tau=c["tau"])
+            ctx64.set_stream(stream)
+            ms_64 = timed(lambda: ctx64.step(fa, fb, dt), reps)
+            ctx64.check()
+            ach64 = flops_per_cell(dv, N, 64) * ncells / (ms_64 * 1e-3) / 1e12
+            extra["A64_step"] = {"value": ncells / (ms_64 * 1e-3), "unit": "cells/s", "ms": ms_64,
+                                 "fp64_frac": ach64 / FP64_PEAK_TFLOPS,
+                                 "what": "fks_step with the 8x8 product direction grid (A = 64), same cells"}
+            ctx64.close()
         if c["dx_dim"] > 0:
             ms_t = timed(lambda: ctx.transport(fa, fb, dt), reps)
             gbs = 2 * ncells * n * 8 / (ms_t * 1e-3) / 1e9
