@@ -353,6 +353,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
     else __syncwarp();
   };
   uint32_t tphase = 0;  // bit b: parity of this group's table buffer b
+  unsigned pub = 0;     // this warp's first z item not yet published
   unsigned seq = 0;     // exchange-buffer sequence index of the next item
   unsigned ncell = 0;   // cells done by this group
   for (int it = cid; it < p.ncells; it += c.ncl, ++ncell) {
@@ -372,6 +373,9 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
     {  // a3 + a4: gather f* (own j_z planes), forward FFT in x and y -> W[s_fwd % NB]
       double2* pln = c.tbuf;  // both table buffers: one plane slab
       constexpr int PER = NP * N * N / GT;  // = N elements per thread
+#ifndef FKS_PUB
+#define FKS_PUB 1  // z items published per release fence (batches of 2 measured slower: the xy group waits)
+#endif
 #ifndef FKS_GATHER_B
 #define FKS_GATHER_B 32  // f* loads in flight per thread in the forward gather (one L2 round trip)
 #endif
@@ -496,6 +500,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       TSTAMPB(10);
       if (tg == 0) sync_signal_relaxed_n(&gs->cons[slot], NW);
       seq = s_fwd + 1;
+      pub = seq;  // first z item of this cell
     }
 #pragma unroll 1
     for (int j = 0; j < D; ++j) {
@@ -514,16 +519,23 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       if (tg_leader && j + 2 < D) load_tab(j + 2);  // into the buffer just freed
       if (lane == 0) {
         if (use > 0) sync_wait_free(&gs->cons[slot], WP * use, cons_seen);
-        // publish this warp's z(j-1): its stores had a whole z pass to drain (cheap release)
-        if (j > 0) sync_signal(&gs->prod[(seq - 1) % NB]);
+        // Publish this warp's z items in batches of FKS_PUB: one release fence (which waits for the
+        // SM's outstanding stores, ~1-2k cycles) per batch, then relaxed adds.
+        if (seq - pub >= FKS_PUB) {
+          asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+          for (; pub < seq; ++pub) sync_signal_relaxed(&gs->prod[pub % NB]);
+        }
       }
       __syncwarp();
       zpass_store<N, P>(x, c.W + slot * C::WBUF, ly, tx);
       TSTAMP(2048 + j * 8 + 3);
       ++seq;
     }
-    __syncwarp();  // this warp's z(D-1) stores precede the release
-    if (lane == 0) sync_signal(&gs->prod[(seq - 1) % NB]);
+    __syncwarp();  // this warp's last stores precede the release
+    if (lane == 0) {
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+      for (; pub < seq; ++pub) sync_signal_relaxed(&gs->prod[pub % NB]);
+    }
     named_bar(1, GT);  // every warp done with the tables before the next forward reuses them
   }
 }
