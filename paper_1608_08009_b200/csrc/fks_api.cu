@@ -227,6 +227,9 @@ struct fks_ctx {
   const double* halo[2] = {nullptr, nullptr};  // caller-owned neighbour planes (FKS_BC_HALO)
   double* d_host_in = nullptr;
   double* d_host_out = nullptr;
+  // fks_step_host pipeline (0D, no solids): copy streams and per-chunk events
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
   int64_t launches = 0;
 };
 
@@ -572,12 +575,69 @@ fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   }
   fks::StepParams p = base_params(c, f_in, f_out, 1);
   fill_transport(c, &p.tp, true);
-  p.cell_list = c->d_fluid;
+  p.cell_list = c->nsolid ? c->d_fluid : nullptr;  // identity list: let the kernels prefetch
   p.ncells = c->nfluid;
   st = run_collision(c, p);
   if (st != FKS_OK) return st;
   c->step_n++;
   return FKS_OK;
+}
+
+// fks_step_host for independent cells (dx = 0, no solids): the batch is cut into chunks and
+// chunk i's step overlaps the host->device copy of chunk i+1 and the device->host copy of
+// chunk i-1 (two copy streams + events; PCIe is full duplex), so the end-to-end time tends to
+// the slowest of the three instead of their sum.
+static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, double* f_out_host, double dt) {
+  fks_status st = check_dt(c, dt);
+  if (st != FKS_OK) return st;
+  const int64_t n = c->n;
+  const int64_t per_round = c->dv == 3 ? (int64_t)std::max(1, c->nclusters) : (int64_t)c->sm_count * fks::cells_per_block2d(c->N);
+  int64_t chunk = std::max<int64_t>(per_round * 2, (c->ncells + 11) / 12);
+  chunk = (chunk + per_round - 1) / per_round * per_round;  // whole rounds of the persistent grid
+  const int nch = (int)((c->ncells + chunk - 1) / chunk);
+  if (!c->s_h2d) {
+    if (cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+      return FKS_E_CUDA;
+  }
+  while ((int)c->ev_in.size() < nch) {
+    cudaEvent_t a, b;
+    if (cudaEventCreateWithFlags(&a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b, cudaEventDisableTiming) != cudaSuccess)
+      return FKS_E_CUDA;
+    c->ev_in.push_back(a);
+    c->ev_out.push_back(b);
+  }
+  cudaEvent_t start;  // the copies must not overtake work already queued on the context stream
+  if (cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess) return FKS_E_CUDA;
+  cudaEventRecord(start, c->stream);
+  cudaStreamWaitEvent(c->s_h2d, start, 0);
+  cudaStreamWaitEvent(c->s_d2h, start, 0);
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < nch && e == cudaSuccess; ++i) {
+    const int64_t off = (int64_t)i * chunk, cnt = std::min(chunk, c->ncells - off);
+    const size_t bytes = (size_t)cnt * n * sizeof(double);
+    e = cudaMemcpyAsync(c->d_host_in + off * n, f_in_host + off * n, bytes, cudaMemcpyHostToDevice, c->s_h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_in[i], c->s_h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, c->ev_in[i], 0);
+    if (e != cudaSuccess) break;
+    fks::StepParams p = base_params(c, c->d_host_in + off * n, c->d_host_out + off * n, 1);
+    fill_transport(c, &p.tp, true);
+    p.cell_list = nullptr;
+    p.ncells = (int)cnt;
+    st = run_collision(c, p);
+    if (st != FKS_OK) break;
+    e = cudaEventRecord(c->ev_out[i], c->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_d2h, c->ev_out[i], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(f_out_host + off * n, c->d_host_out + off * n, bytes, cudaMemcpyDeviceToHost, c->s_d2h);
+  }
+  cudaEventDestroy(start);
+  if (st != FKS_OK) return st;
+  if (e != cudaSuccess) return FKS_E_CUDA;
+  c->step_n++;
+  if (cudaStreamSynchronize(c->s_d2h) != cudaSuccess) return FKS_E_CUDA;
+  return cuda_fail(cudaStreamSynchronize(c->stream));
 }
 
 fks_status fks_step_host(fks_ctx* c, const double* f_in_host, double* f_out_host, double dt) {
@@ -587,6 +647,7 @@ fks_status fks_step_host(fks_ctx* c, const double* f_in_host, double* f_out_host
     if (cudaMalloc(&c->d_host_in, bytes) != cudaSuccess) return FKS_E_NOMEM;
     if (cudaMalloc(&c->d_host_out, bytes) != cudaSuccess) return FKS_E_NOMEM;
   }
+  if (c->grid.dx == 0 && c->nsolid == 0) return step_host_pipelined(c, f_in_host, f_out_host, dt);
   if (cudaMemcpyAsync(c->d_host_in, f_in_host, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     return FKS_E_CUDA;
   fks_status st = fks_step(c, c->d_host_in, c->d_host_out, dt);
@@ -641,6 +702,10 @@ fks_status fks_finalize(fks_ctx* c) {
   cudaFree(c->d_solid_list);
   cudaFree(c->d_solid);
   for (auto& g : c->d_ghost) cudaFree(g);
+  for (cudaEvent_t ev : c->ev_in) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->ev_out) cudaEventDestroy(ev);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   cudaFree(c->d_host_in);
   cudaFree(c->d_host_out);
   delete c;

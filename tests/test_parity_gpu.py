@@ -301,6 +301,23 @@ def test_deterministic_and_host_path(torch, fks):
     np.testing.assert_array_equal(hout.numpy(), outs[0])
 
 
+@pytest.mark.parametrize("dv,N,ncells", [(3, 8, 311), (2, 16, 5003)])
+def test_host_path_pipelined_chunks(torch, fks, dv, N, ncells):
+    """fks_step_host on a batch that spans several copy/compute chunks (ragged last chunk) is
+    bitwise the device fks_step."""
+    L = 6.0
+    f = workloads.family("smooth", dv, N, L, ncells, seed=31)
+    A = 24 if dv == 3 else 8
+    ctx = fks.Context(dv, 0, [ncells], N, L, A)
+    o = torch.empty((ncells,) + (N,) * dv, dtype=torch.float64, device="cuda")
+    ctx.step(dev(torch, f), o, 0.05)
+    ctx_h = fks.Context(dv, 0, [ncells], N, L, A)
+    hin = torch.from_numpy(f.copy()).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    ctx_h.step_host(hin, hout, 0.05)
+    np.testing.assert_array_equal(hout.numpy(), host(o))
+
+
 def test_full_size_C2_launch_sampled(torch, fks):
     """BASELINE configs[1] at full size (4096 cells) in bench.py's launch configuration; sampled
     cells against the oracle one by one, plus exact mass conservation on every cell."""
