@@ -117,7 +117,10 @@ fks_status fks_transport(fks_ctx* ctx, const double* f_in, double* f_out, double
 fks_status fks_step(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
 
 /* fks_step with HOST buffers: copies f_in_host to the device, steps, copies the result back
- * to f_out_host and synchronises the stream (end-to-end path; pinned memory recommended). */
+ * to f_out_host and synchronises (end-to-end path; pinned memory recommended).  For independent
+ * cells (dx = 0, no solids) the batch is processed in chunks so that the host->device copy, the
+ * step and the device->host copy of consecutive chunks overlap (two library-owned copy
+ * streams); the result is bitwise that of fks_step. */
 fks_status fks_step_host(fks_ctx* ctx, const double* f_in_host, double* f_out_host, double dt);
 
 /* a10: rho[cell], u[cell][dv], T[cell] (T = int |v-u|^2 f / (dv rho), reading #12). */
