@@ -123,6 +123,15 @@ fks_status fks_step(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
  * streams); the result is bitwise that of fks_step. */
 fks_status fks_step_host(fks_ctx* ctx, const double* f_in_host, double* f_out_host, double dt);
 
+/* NEXT-2 (beyond the Boltzmann hot path): one BGK step, F = f* + (dt/tau) nu (E[f*] - f*), with
+ * the transport gather of fks_step (a1+a3) and the conservative Maxwellian E of eq. minimMax
+ * (the Maxwellian of the cell's moments projected onto them, so mass, momentum and
+ * energy are exact).  nu_rule: FKS_NU_RHO (nu = rho), FKS_NU_CONST (nu = mu > 0),
+ * FKS_NU_EULER (the tau -> 0 limit, F = E[f*]).  tau from fks_set_params.  Advances the step
+ * counter like fks_step; solid cells are copied.  Device pointers, f_out != f_in. */
+enum { FKS_NU_RHO = 0, FKS_NU_CONST = 1, FKS_NU_EULER = 2 };
+fks_status fks_step_bgk(fks_ctx* ctx, const double* f_in, double* f_out, double dt, int nu_rule, double mu);
+
 /* a10: rho[cell], u[cell][dv], T[cell] (T = int |v-u|^2 f / (dv rho), reading #12). */
 fks_status fks_moments(fks_ctx* ctx, const double* f, double* rho, double* u, double* T);
 

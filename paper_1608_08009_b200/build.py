@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfks.so")
-SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels3d.cu", "kernels_aux.cu"]
+SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels3d.cu", "kernels_aux.cu", "kernels_bgk.cu"]
 HEADERS = ["fft.cuh", "common.cuh", "kernels.cuh", os.path.join("..", "..", "include", "fks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + os.environ.get("FKS_NVCC_EXTRA", "").split() + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

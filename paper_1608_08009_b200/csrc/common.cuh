@@ -37,6 +37,21 @@ struct StepParams {
   TransportParams tp;
 };
 
+// NEXT-2 BGK step (kernels_bgk.cu).
+struct BgkParams {
+  const double* f_in;
+  double* f_out;
+  int* nonfinite;
+  const int* cell_list;  // fluid cells (nullptr: all)
+  int ncells;
+  int nu_rule;           // 0: nu = rho, 1: nu = mu, 2: Euler limit (F = E[f*])
+  double mu;
+  double dt_tau;
+  double L, dv;
+  double Ginv[25];       // (Phi Phi^T)^{-1}, (dv+2)^2 row-major
+  TransportParams tp;
+};
+
 // Coordinates of a local cell along each space axis (computed once per cell, not per element).
 struct CellCoord {
   int j[3];

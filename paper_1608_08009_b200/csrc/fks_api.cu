@@ -583,6 +583,37 @@ fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   return FKS_OK;
 }
 
+fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt, int nu_rule, double mu) {
+  if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
+  if (nu_rule < FKS_NU_RHO || nu_rule > FKS_NU_EULER || (nu_rule == FKS_NU_CONST && !(mu > 0))) return FKS_E_INVAL;
+  fks_status st = check_dt(c, dt);
+  if (st != FKS_OK) return st;
+  if (c->nsolid) {
+    if (fks::launch_copy_cells(f_in, f_out, c->d_solid_list, c->nsolid, c->n, c->stream) != cudaSuccess)
+      return FKS_E_CUDA;
+    c->launches++;
+  }
+  fks::BgkParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.f_in = f_in;
+  p.f_out = f_out;
+  p.nonfinite = c->d_flag;
+  p.cell_list = c->nsolid ? c->d_fluid : nullptr;
+  p.ncells = c->nfluid;
+  p.nu_rule = nu_rule;
+  p.mu = mu;
+  p.dt_tau = c->dt / c->tau;
+  p.L = c->L;
+  p.dv = 2.0 * c->L / c->N;
+  std::memcpy(p.Ginv, c->Ginv, sizeof(p.Ginv));
+  fill_transport(c, &p.tp, true);
+  cudaError_t e = fks::launch_bgk(c->N, c->dv, p, c->sm_count, c->stream);
+  c->launches++;
+  if (e != cudaSuccess) return FKS_E_CUDA;
+  c->step_n++;
+  return FKS_OK;
+}
+
 // fks_step_host for independent cells (dx = 0, no solids): the batch is cut into chunks and
 // chunk i's step overlaps the host->device copy of chunk i+1 and the device->host copy of
 // chunk i-1 (two copy streams + events; PCIe is full duplex), so the end-to-end time tends to

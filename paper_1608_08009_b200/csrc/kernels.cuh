@@ -27,6 +27,9 @@ cudaError_t launch_transport(const double* f_in, double* f_out, const TransportP
 // Copy the listed cells f_out[c] = f_in[c] (solid cells in fks_step).
 cudaError_t launch_copy_cells(const double* f_in, double* f_out, const int* cells, int count, int n, cudaStream_t s);
 
+// NEXT-2: BGK relaxation step (transport gather + conservative Maxwellian + forward Euler).
+cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStream_t s);
+
 // a10: rho, u[dv], T per cell.
 cudaError_t launch_moments(const double* f, double* rho, double* u, double* T, int64_t ncells, int N, int dv,
                            double L, double dv_spacing, cudaStream_t s);

@@ -11,6 +11,7 @@ import numpy as np
 from ._lib import FksError, FksGrid, check, load  # noqa: F401
 
 BC_PERIODIC, BC_GHOST, BC_OUTFLOW, BC_HALO = 0, 1, 2, 3
+NU_RHO, NU_CONST, NU_EULER = 0, 1, 2  # fks_step_bgk collision-frequency rules (include/fks.h)
 
 
 def _ptr(t):
@@ -95,6 +96,11 @@ class Context:
 
     def step(self, f_in, f_out, dt):
         check(self._lib.fks_step(self.handle, _ptr(f_in), _ptr(f_out), float(dt)), "fks_step")
+
+    def step_bgk(self, f_in, f_out, dt, nu_rule=0, mu=0.0):
+        """NEXT-2: one BGK step (fks_step_bgk); nu_rule NU_RHO / NU_CONST (mu) / NU_EULER."""
+        check(self._lib.fks_step_bgk(self.handle, _ptr(f_in), _ptr(f_out), float(dt), int(nu_rule), float(mu)),
+              "fks_step_bgk")
 
     def step_host(self, f_in, f_out, dt):
         """f_in, f_out: host float64 arrays/tensors (pinned recommended); synchronous."""

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import workloads
-from oracle import collision, grid, moments, projection, step as ostep, tables, transport
+from oracle import bgk, collision, grid, moments, projection, step as ostep, tables, transport
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-11
@@ -251,6 +251,59 @@ def test_collide_3d_one_group_many_cells(torch, fks, N, L, ncells, monkeypatch):
     ref = ostep.homogeneous_step(f, tab, c["dt"])
     got = host(g)
     for i in range(ncells):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
+# ---------------------------------------------------------------- NEXT-2: BGK step
+@pytest.mark.parametrize("dv,N,L,kind", [(2, 32, 9.0, "bkw"), (2, 16, 6.0, "random"), (3, 16, 7.0, "smooth"),
+                                         (3, 32, 7.0, "random")])
+@pytest.mark.parametrize("nu_rule,mu", [(bgk.NU_RHO, 0.0), (bgk.NU_CONST, 1.7), (bgk.NU_EULER, 0.0)])
+def test_bgk_step_0d(torch, fks, dv, N, L, kind, nu_rule, mu):
+    ncells = 9 if dv == 3 else 37
+    f = workloads.family(kind, dv, N, L, ncells, seed=41)
+    ctx = fks.Context(dv, 0, [ncells], N, L, 8 if dv == 2 else 24)
+    ctx.set_params(tau=0.8)
+    out = torch.empty_like(dev(torch, f))
+    dt = 0.05
+    ctx.step_bgk(dev(torch, f), out, dt, nu_rule, mu)
+    ctx.check()
+    ref = bgk.homogeneous_bgk_step(f, dt, 0.8, nu_rule, mu, dv, N, L)
+    got = host(out)
+    for i in range(ncells):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
+@pytest.mark.parametrize("dxd,dv,M,N,bc", [
+    (1, 3, [9], 8, [transport.GHOST, transport.OUTFLOW]),
+    (2, 2, [5, 4], 16, [transport.GHOST, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC]),
+])
+def test_bgk_step_with_transport(torch, fks, dxd, dv, M, N, bc):
+    """Two fused BGK steps (gather + conservative Maxwellian + Euler) with ghosts and a solid cell,
+    against the oracle's transport followed by its per-cell BGK step."""
+    L = 6.0
+    F, h, dt, ghosts = _spatial_case(dxd, dv, M, N, L, bc, seed=3)
+    solid = np.zeros(tuple(M[::-1]), dtype=bool)
+    solid.reshape(-1)[int(np.prod(M)) // 2] = True
+    ctx = fks.Context(dv, dxd, M, N, L, 8 if dv == 2 else 24, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_solid(solid)
+    ctx.set_params(tau=0.5)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    vshape = (N,) * dv
+    for s in range(2):
+        ctx.step_bgk(a, b, dt, bgk.NU_RHO, 0.0)
+        a, b = b, a
+        fstar = transport.gather(ref, s, dxd, dv, N, L, dt, h, bc, ghosts)
+        nxt = np.empty_like(ref)
+        for j in range(int(np.prod(M))):
+            idx = np.unravel_index(j, tuple(M[::-1]))
+            nxt[idx] = ref[idx] if solid[idx] else bgk.bgk_step_cell(fstar[idx], dt, 0.5, bgk.NU_RHO, 0.0, dv, N, L)
+        ref = nxt
+    got = host(a).reshape((-1,) + vshape)
+    ref = ref.reshape((-1,) + vshape)
+    for i in range(ref.shape[0]):
         assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
 
 
