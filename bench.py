@@ -318,6 +318,21 @@ def main():
                                        "hbm_gbs": gbs, "hbm_peak_gbs": peak,
                                        "hbm_frac": gbs / peak if peak else None,
                                        "what": "fks_transport (a1+a3, 16 B per phase-space update), HBM-bound"}
+        # NEXT-2: the BGK step on the same cells (nu = rho), HBM-bound (16 B per update)
+        ctxb = fks.Context(dv, c["dx_dim"], [ncells] if c["dx_dim"] == 0 else list(slab.M_local), N, c["L"], A,
+                           **({} if c["dx_dim"] == 0 else dict(h=c["dx"], bc=slab.local_bc(c["bc"]))))
+        if c["dx_dim"] > 0:
+            for face, g in workloads.ghost_vectors(c).items():
+                ctxb.set_ghost(face, torch.from_numpy(g).cuda())
+        ctxb.set_params(tau=c["tau"])
+        ctxb.set_stream(stream)
+        ms_b = timed(lambda: ctxb.step_bgk(fa, fb, dt, fks.NU_RHO, 0.0), reps)
+        ctxb.check()
+        gbs = 2 * ncells * n * 8 / (ms_b * 1e-3) / 1e9
+        extra["bgk_step"] = {"value": ncells / (ms_b * 1e-3), "unit": "cells/s", "ms": ms_b, "hbm_gbs": gbs,
+                             "hbm_frac": gbs / hbm_peak(),
+                             "what": "NEXT-2 fks_step_bgk (transport + conservative Maxwellian + Euler, nu = rho)"}
+        ctxb.close()
         rho = torch.empty(ncells, dtype=torch.float64, device=fa.device)
         uu = torch.empty(ncells, dv, dtype=torch.float64, device=fa.device)
         TT = torch.empty(ncells, dtype=torch.float64, device=fa.device)

@@ -7,7 +7,8 @@
 // evaluates the pointwise Maxwellian and reduces its moments, pass 3 writes
 // f* + (dt/tau) nu (E - f*).  f* is re-gathered (an L2 hit) instead of held: a 32^3 cell is
 // 256 KiB.  Reductions are fixed-order (warp shuffles, then warps in order): deterministic.
-// HBM-bound: 16 B per phase-space update (read f, write f) plus two FP64 exp per node.
+// HBM-bound: 16 B per phase-space update (read f, write f); the Maxwellian is separable, so a
+// cell needs only DV * N exponentials.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
   __shared__ int8_t sdelta[3][kMaxN];
   __shared__ const double* sbase[27];
   __shared__ double red[8][5];
+  __shared__ double sexp[3][kMaxN];  // separable Maxwellian factors exp(-(v_k - u_a)^2 / (2T))
   load_delta(p.tp, sdelta);
   const double h = p.dv;
   double vol = 1.0;
@@ -96,10 +98,16 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
     }
     const double T = (vol * m[4] / rho - uu) / DV;
     const double amp = rho / pow(2.0 * 3.141592653589793 * T, 0.5 * DV);
+    // the Maxwellian is a product of 1D Gaussians: DV * N exponentials per cell, not n
+    if (threadIdx.x < DV * N) {
+      const int a = threadIdx.x / N, k = threadIdx.x % N;
+      const double w = node_v(k, p.L, h) - u[a];
+      sexp[a][k] = exp(-(w * w) / (2.0 * T));
+    }
+    __syncthreads();
     auto maxw = [&](int k) -> double {  // pointwise Maxwellian E~
-      const double vx = node_v(k % N, p.L, h) - u[0], vy = node_v((k / N) % N, p.L, h) - u[1];
-      const double vz = DV == 3 ? node_v(k / (N * N), p.L, h) - u[2] : 0.0;
-      return amp * exp(-(vx * vx + vy * vy + vz * vz) / (2.0 * T));
+      const double e = amp * sexp[0][k % N] * sexp[1][(k / N) % N];
+      return DV == 3 ? e * sexp[2][k / (N * N)] : e;
     };
     // pass 2: moments of E~, then lambda = (Phi Phi^T)^{-1} (Phi f* - Phi E~)
     double me[5] = {0, 0, 0, 0, 0};
