@@ -76,14 +76,31 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
       }
       return gather_fstar(p.f_in, p.tp, cc, k, kx, ky, kz, n, sdelta);
     };
-    // pass 1: moments of f*
+    // the next cell of this CTA (homogeneous case: contiguous) -> L2 while this one is processed
+    if (p.tp.dx == 0 && threadIdx.x == 0 && !p.cell_list && it + gridDim.x < p.ncells)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.f_in + (int64_t)(it + gridDim.x) * n),
+                   "r"((uint32_t)(n * sizeof(double)))
+                   : "memory");
+    // pass 1: moments of f* (homogeneous cells: 16-byte loads, two velocities per thread)
     double m[5] = {0, 0, 0, 0, 0};
-    for (int k = threadIdx.x; k < n; k += 256) {
-      const double f = fstar(k);
-      double ph[5];
-      phi_row<N, DV>(k, p.L, h, ph);
+    if (p.tp.dx == 0) {
+      const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * n);
+      for (int k2 = threadIdx.x; k2 < n / 2; k2 += 256) {
+        const double2 f2 = __ldg(src + k2);
+        double ph[5], pq[5];
+        phi_row<N, DV>(2 * k2, p.L, h, ph);
+        phi_row<N, DV>(2 * k2 + 1, p.L, h, pq);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) m[c] = fma(ph[c], f, m[c]);
+        for (int c = 0; c < 5; ++c) m[c] = fma(pq[c], f2.y, fma(ph[c], f2.x, m[c]));
+      }
+    } else {
+      for (int k = threadIdx.x; k < n; k += 256) {
+        const double f = fstar(k);
+        double ph[5];
+        phi_row<N, DV>(k, p.L, h, ph);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) m[c] = fma(ph[c], f, m[c]);
+      }
     }
     block_sum5(m, red);
     double U[5];  // Phi f* in the row order 1, v_x .. v_{DV-1}, |v|^2
@@ -134,16 +151,108 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
     // pass 3: E = E~ + Phi^T lambda; F = f* + (dt/tau) nu (E - f*)  (or E: Euler limit)
     bool bad = false;
     double* out = p.f_out + cell * n;
-    for (int k = threadIdx.x; k < n; k += 256) {
+    auto update = [&](int k, double f) {
       double ph[5];
       phi_row<N, DV>(k, p.L, h, ph);
       double E = maxw(k) + lam[0];
       for (int a = 0; a < DV; ++a) E = fma(lam[1 + a], ph[1 + a], E);
       E = fma(lam[DV + 1], ph[4], E);
-      const double f = fstar(k);
       const double o = p.nu_rule == 2 ? E : fma(c1, E - f, f);
       bad |= !isfinite(o);
-      out[k] = o;
+      return o;
+    };
+    if (p.tp.dx == 0) {
+      const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * n);
+      double2* dst = reinterpret_cast<double2*>(out);
+      for (int k2 = threadIdx.x; k2 < n / 2; k2 += 256) {
+        const double2 f2 = __ldg(src + k2);
+        const double o0 = update(2 * k2, f2.x), o1 = update(2 * k2 + 1, f2.y);
+        dst[k2] = make_double2(o0, o1);
+      }
+    } else {
+      for (int k = threadIdx.x; k < n; k += 256) out[k] = update(k, fstar(k));
+    }
+    if (bad) atomicOr(p.nonfinite, 1);
+  }
+}
+
+// 2D cells (N^2 <= 1024 nodes): one warp per cell, homogeneous (dx = 0) only; reductions are
+// warp shuffles in a fixed order.  Same arithmetic as k_bgk.
+template <int N>
+__global__ void __launch_bounds__(256) k_bgk2w(const BgkParams p) {
+  constexpr int n = N * N;
+  __shared__ double sexp[8][2][N];
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+  const double h = p.dv, vol = h * h;
+  for (int it = blockIdx.x * 8 + wv; it < p.ncells; it += gridDim.x * 8) {
+    const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * n);
+    double m[5] = {0, 0, 0, 0, 0};
+    for (int k2 = lane; k2 < n / 2; k2 += 32) {
+      const double2 f2 = __ldg(src + k2);
+      double ph[5], pq[5];
+      phi_row<N, 2>(2 * k2, p.L, h, ph);
+      phi_row<N, 2>(2 * k2 + 1, p.L, h, pq);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) m[c] = fma(pq[c], f2.y, fma(ph[c], f2.x, m[c]));
+    }
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
+    }
+    const double rho = vol * m[0];
+    const double u0 = vol * m[1] / rho, u1 = vol * m[2] / rho;
+    const double T = (vol * m[4] / rho - (u0 * u0 + u1 * u1)) / 2;
+    const double amp = rho / pow(2.0 * 3.141592653589793 * T, 1.0);
+    __syncwarp();
+    for (int i = lane; i < 2 * N; i += 32) {
+      const int a = i / N, k = i % N;
+      const double w = node_v(k, p.L, h) - (a == 0 ? u0 : u1);
+      sexp[wv][a][k] = exp(-(w * w) / (2.0 * T));
+    }
+    __syncwarp();
+    auto maxw = [&](int k) { return amp * sexp[wv][0][k % N] * sexp[wv][1][k / N]; };
+    double me[5] = {0, 0, 0, 0, 0};
+    for (int k = lane; k < n; k += 32) {
+      const double e = maxw(k);
+      double ph[5];
+      phi_row<N, 2>(k, p.L, h, ph);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) me[c] = fma(ph[c], e, me[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) me[c] += __shfl_xor_sync(0xffffffffu, me[c], o);
+    }
+    const double r[4] = {m[0] - me[0], m[1] - me[1], m[2] - me[2], m[4] - me[4]};
+    double lam[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) sacc = fma(p.Ginv[a * 4 + b], r[b], sacc);
+      lam[a] = sacc;
+    }
+    const double c1 = p.dt_tau * (p.nu_rule == 0 ? rho : p.mu);
+    bool bad = false;
+    auto update = [&](int k, double f) {
+      double ph[5];
+      phi_row<N, 2>(k, p.L, h, ph);
+      double E = maxw(k) + lam[0];
+      E = fma(lam[1], ph[1], E);
+      E = fma(lam[2], ph[2], E);
+      E = fma(lam[3], ph[4], E);
+      const double o = p.nu_rule == 2 ? E : fma(c1, E - f, f);
+      bad |= !isfinite(o);
+      return o;
+    };
+    double2* dst = reinterpret_cast<double2*>(p.f_out + cell * n);
+    for (int k2 = lane; k2 < n / 2; k2 += 32) {
+      const double2 f2 = __ldg(src + k2);
+      const double o0 = update(2 * k2, f2.x), o1 = update(2 * k2 + 1, f2.y);
+      dst[k2] = make_double2(o0, o1);
     }
     if (bad) atomicOr(p.nonfinite, 1);
   }
@@ -151,6 +260,12 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
 
 cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStream_t s) {
   if (p.ncells == 0) return cudaSuccess;
+  if (dv == 2 && p.tp.dx == 0) {
+    const unsigned nw = (unsigned)((p.ncells + 7) / 8 < sm_count * 8 ? (p.ncells + 7) / 8 : sm_count * 8);
+    if (N == 8) { k_bgk2w<8><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
+    if (N == 16) { k_bgk2w<16><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
+    if (N == 32) { k_bgk2w<32><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
+  }
   const unsigned nb = (unsigned)(p.ncells < sm_count * 8 ? p.ncells : sm_count * 8);
 #define FKS_BGK(NN, DD) \
   if (N == NN && dv == DD) { k_bgk<NN, DD><<<nb, 256, 0, s>>>(p); return cudaGetLastError(); }
