@@ -84,3 +84,74 @@ def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None, cells=None):
         else:
             sub[pos] = vals
     return out if sub is None else sub
+
+
+def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid):
+    """NEXT-1: f* with specular reflection at solid cells ("reflective boundary conditions",
+    S:430-438 apply_solid_reflection; reading #23 of DESIGN.md).
+
+    Forward picture: a particle of velocity index k moves axis by axis (axis 0 first) by its
+    shift; when the next cell along an axis is solid it is reflected instead (v_a -> -v_a, on the
+    symmetric lattice k_a -> N-1-k_a) and stays.  The gather inverts that map, so in a closed box
+    it is a permutation of the fluid values (mass and energy conserved exactly).  For a fluid cell
+    j and arrived velocity k, undo the axes in reverse order (dxd-1 .. 0) from c = j:
+      the candidate origin along a is c + delta_a(k_a) e_a (wrapped on a PERIODIC face); if it is an
+      in-domain solid cell the particle was reflected there: k_a -> N-1-k_a and c stays;
+      otherwise c moves to it.
+    The value is then read as in gather() from the source j + (the shifts of the axes that were not
+    reflected), with the face rules (GHOST / OUTFLOW / PERIODIC), at the mirrored index k'.  Without
+    solids this is exactly gather().  Solid cells keep their values.  Plain scalar loops."""
+    sp_shape = F.shape[:dxd]
+    M = sp_shape[::-1]
+    delta = shift_delta(n, N, L, dt, dx)
+    out = np.empty_like(F)
+
+    def in_domain_solid(cell):                               # cell: list of dxd coordinates
+        if any(c < 0 or c >= M[a] for a, c in enumerate(cell)):
+            return False
+        return bool(solid[tuple(cell[dxd - 1 - b] for b in range(dxd))])
+
+    for jflat in range(int(np.prod(sp_shape))):
+        jidx = np.unravel_index(jflat, sp_shape)
+        if solid[jidx]:
+            out[jidx] = F[jidx]
+            continue
+        j = [jidx[dxd - 1 - a] for a in range(dxd)]
+        for kidx in np.ndindex(*((N,) * dv)):
+            kc = [kidx[dv - 1 - a] for a in range(dv)]      # velocity component a
+            d = [int(delta[kc[a]]) for a in range(dxd)]
+            flip = [False] * dv
+            c = list(j)
+            for a in reversed(range(dxd)):
+                if d[a] == 0:
+                    continue
+                nb = list(c)
+                nb[a] = c[a] + d[a]
+                if bc[2 * a if d[a] < 0 else 2 * a + 1] == PERIODIC:
+                    nb[a] %= M[a]
+                if in_domain_solid(nb):
+                    flip[a], d[a] = True, 0
+                else:
+                    c = nb
+            # the source after the face rules (as gather(): lowest axis with a ghost face wins)
+            s, gface = list(j), -1
+            for a in range(dxd):
+                v = j[a] + d[a]
+                if v < 0 or v >= M[a]:
+                    face = 2 * a if v < 0 else 2 * a + 1
+                    kind = bc[face]
+                    if kind == PERIODIC:
+                        v %= M[a]
+                    else:
+                        if kind == GHOST and gface < 0:
+                            gface = face
+                        v = min(max(v, 0), M[a] - 1)
+                s[a] = v
+            kp = [N - 1 - kc[a] if flip[a] else kc[a] for a in range(dv)]
+            kpidx = tuple(kp[dv - 1 - b] for b in range(dv))
+            if gface >= 0:
+                val = ghosts[gface][kpidx]
+            else:
+                val = F[tuple(s[dxd - 1 - b] for b in range(dxd)) + kpidx]
+            out[jidx + kidx] = val
+    return out
