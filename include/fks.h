@@ -102,6 +102,14 @@ fks_status fks_set_halo(fks_ctx* ctx, const double* lo_plane, const double* hi_p
  * their values (reading #19; specular reflection is NEXT work). NULL clears it. */
 fks_status fks_set_solid(fks_ctx* ctx, const uint8_t* solid_host);
 
+/* NEXT-1: specular reflection at solid cells instead of the frozen solid values of reading #19
+ * ("reflective boundary conditions"; reading #23): in the transport gather of
+ * fks_transport / fks_step / fks_step_bgk, a particle whose per-axis move would end in a solid
+ * cell is reflected there (velocity component mirrored, k_a -> N-1-k_a) -- the inverse of the
+ * forward bounce map, so a closed box conserves mass and energy exactly.  on = 0 restores the
+ * default.  FKS_E_UNSUPPORTED with HALO faces (a partitioned grid). */
+fks_status fks_set_specular(fks_ctx* ctx, int on);
+
 /* Stream (a cudaStream_t passed as void*) on which all later work is enqueued. */
 fks_status fks_set_stream(fks_ctx* ctx, void* cuda_stream);
 

@@ -13,6 +13,9 @@ struct TransportParams {
   int M[3];                // local cells per space axis (axis 0 fastest)
   int bc[6];               // FKS_BC_* per face
   int cfl1;                // every |delta| <= 1 (the 3^dx-sources fast paths apply)
+  int reflect;             // NEXT-1: specular reflection at solid cells (needs solid)
+  int Nv;                  // velocity nodes per axis (mirror index N-1-k)
+  const uint8_t* solid;    // [local cells] solid mask (nullptr: none)
   int8_t delta[3][kMaxN];  // delta[a][k_a] = s^{n+1} - s^n for velocity component a
   const double* ghost[6];  // ghost vectors (n values) of GHOST faces, device memory
   const double* halo[2];   // HALO faces of the slowest axis: neighbour rank's boundary plane
@@ -114,11 +117,58 @@ __device__ __forceinline__ const double* source_base(const double* __restrict__ 
   return F + src * n;
 }
 
+// NEXT-1 (specular reflection, oracle/transport.gather_specular): undo the per-axis moves in
+// reverse axis order from cell j; a move whose origin is an in-domain solid cell was a reflection
+// instead (component a mirrored, no move).  Returns the source of the remaining shifts (face rules
+// of source_base) and the mask of mirrored velocity components.
+__device__ __forceinline__ const double* source_resolve(const double* __restrict__ F, const TransportParams& tp,
+                                                        const CellCoord& cc, int (&d)[3], int n, int& flip) {
+  flip = 0;
+  if (tp.reflect) {
+    int c[3] = {cc.j[0], cc.j[1], cc.j[2]};
+#pragma unroll
+    for (int a = 2; a >= 0; --a) {
+      if (a >= tp.dx || d[a] == 0) continue;
+      int nb = c[a] + d[a];
+      if (tp.bc[d[a] < 0 ? 2 * a : 2 * a + 1] == 0) nb = (nb + tp.M[a]) % tp.M[a];  // PERIODIC
+      bool is_solid = false;
+      if (nb >= 0 && nb < tp.M[a]) {
+        int64_t idx = 0, stride = 1;
+        for (int b = 0; b < tp.dx; ++b) {
+          idx += (int64_t)(b == a ? nb : c[b]) * stride;
+          stride *= tp.M[b];
+        }
+        is_solid = tp.solid[idx] != 0;
+      }
+      if (is_solid) {
+        flip |= 1 << a;
+        d[a] = 0;
+      } else {
+        c[a] = nb;
+      }
+    }
+  }
+  return source_base(F, tp, cc, d, n);
+}
+
+// velocity index k with the components in `flip` mirrored (k_a -> N-1-k_a)
+__device__ __forceinline__ int mirror_k(int k, int kx, int ky, int kz, int flip, int N) {
+  if (flip & 1) k += N - 1 - 2 * kx;
+  if (flip & 2) k += (N - 1 - 2 * ky) * N;
+  if (flip & 4) k += (N - 1 - 2 * kz) * N * N;
+  return k;
+}
+
 __device__ __forceinline__ double gather_fstar(const double* __restrict__ F, const TransportParams& tp,
                                                const CellCoord& cc, int k, int kx, int ky, int kz, int n,
                                                const int8_t (*delta)[kMaxN]) {
   if (tp.dx == 0) return F[cc.cell * n + k];
-  const int d[3] = {delta[0][kx], tp.dx > 1 ? delta[1][ky] : 0, tp.dx > 2 ? delta[2][kz] : 0};
+  int d[3] = {delta[0][kx], tp.dx > 1 ? delta[1][ky] : 0, tp.dx > 2 ? delta[2][kz] : 0};
+  if (tp.reflect) {
+    int flip;
+    const double* base = source_resolve(F, tp, cc, d, n, flip);
+    return base[mirror_k(k, kx, ky, kz, flip, tp.Nv)];
+  }
   return source_base(F, tp, cc, d, n)[k];
 }
 

@@ -223,6 +223,7 @@ struct fks_ctx {
   int* d_solid_list = nullptr;
   int nsolid = 0;
   uint8_t* d_solid = nullptr;
+  int reflect = 0;  // NEXT-1: specular reflection at solid cells
   double* d_ghost[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   const double* halo[2] = {nullptr, nullptr};  // caller-owned neighbour planes (FKS_BC_HALO)
   double* d_host_in = nullptr;
@@ -330,6 +331,9 @@ void fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift)
   tp->halo[1] = c->halo[1];
   if (with_shift)
     for (int a = 0; a < c->grid.dx; ++a) shift_delta(c->step_n, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
+  tp->solid = c->d_solid;
+  tp->reflect = (c->reflect && c->d_solid && with_shift) ? 1 : 0;
+  tp->Nv = c->N;
   tp->cfl1 = 1;
   for (int a = 0; a < 3; ++a)
     for (int k = 0; k < fks::kMaxN; ++k) tp->cfl1 &= tp->delta[a][k] >= -1 && tp->delta[a][k] <= 1;
@@ -520,6 +524,15 @@ fks_status fks_set_halo(fks_ctx* c, const double* lo_plane, const double* hi_pla
   return FKS_OK;
 }
 
+fks_status fks_set_specular(fks_ctx* c, int on) {
+  if (!c) return FKS_E_INVAL;
+  if (on)
+    for (int f = 0; f < 2 * c->grid.dx; ++f)
+      if (c->grid.bc[f] == FKS_BC_HALO) return FKS_E_UNSUPPORTED;
+  c->reflect = on ? 1 : 0;
+  return FKS_OK;
+}
+
 fks_status fks_set_solid(fks_ctx* c, const uint8_t* solid_host) {
   if (!c) return FKS_E_INVAL;
   return set_cell_lists(c, solid_host);
@@ -542,6 +555,9 @@ fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
 
 static fks_status check_dt(fks_ctx* c, double dt) {
   if (!(dt > 0)) return FKS_E_INVAL;
+  if (c->reflect)  // the neighbour rank's solid cells are not known here
+    for (int f = 0; f < 2 * c->grid.dx; ++f)
+      if (c->grid.bc[f] == FKS_BC_HALO) return FKS_E_UNSUPPORTED;
   for (int f = 0; f < 2 * c->grid.dx; ++f) {
     if (c->grid.bc[f] == FKS_BC_GHOST && !c->d_ghost[f]) return FKS_E_STATE;
     if (c->grid.bc[f] == FKS_BC_HALO && !c->halo[f & 1]) return FKS_E_STATE;

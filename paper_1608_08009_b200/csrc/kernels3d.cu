@@ -83,7 +83,8 @@ struct Cfg3 {
   static constexpr size_t OFF_TMEM = OFF_MBAR + 8 * NMBAR;
   static constexpr size_t OFF_PART = OFF_TMEM + 8;           // lambda[5] + warp partials [4][5]
   static constexpr size_t OFF_SBASE = OFF_PART + 32 * 8;  // [27] transport sources of the cell
-  static constexpr size_t OFF_DELTA = OFF_SBASE + 27 * 8;  // int8 [3][kMaxN] shift table
+  static constexpr size_t OFF_SFLIP = OFF_SBASE + 27 * 8;  // int8 [27] mirrored components
+  static constexpr size_t OFF_DELTA = OFF_SFLIP + 32;      // int8 [3][kMaxN] shift table
   static constexpr size_t SMEM = OFF_DELTA + 3 * kMaxN;
   static_assert(GT % 32 == 0, "warp groups must be whole warps");
   static_assert(NP % 2 == 0, "mirror pairs stay within a CTA");
@@ -309,6 +310,7 @@ struct Ctx3 {
   double* part;    // [8] epilogue scratch (moment sums, lambda)
   const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
   const double** sbase;          // [27] per-cell transport sources (forward gather, dx > 0)
+  int8_t* sflip;                 // [27] their mirrored velocity components (specular reflection)
   double2* W;      // [NBUF][N j_z][N l_y][N l_x] exchange buffers of this group (L2, swizzled)
   GroupSync* gs;   // this group's counters
   int rank, cid, ncl, tg, tx, tl;
@@ -390,8 +392,10 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
         } else if (p.tp.cfl1) {  // sources per shift combination resolved once per cell, then lookups
           if (b0 == 0) {
             if (tg < 27) {
-              const int d[3] = {tg % 3 - 1, (tg / 3) % 3 - 1, tg / 9 - 1};
-              c.sbase[tg] = source_base(p.f_in, p.tp, cc_cell, d, n);
+              int d[3] = {tg % 3 - 1, (tg / 3) % 3 - 1, tg / 9 - 1};
+              int flip = 0;
+              c.sbase[tg] = source_resolve(p.f_in, p.tp, cc_cell, d, n, flip);
+              c.sflip[tg] = (int8_t)flip;
             }
             named_bar(1, GT);
           }
@@ -400,7 +404,8 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
             const int e = tg + (b0 + j) * GT;
             const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
             const int combo = (c.delta[0][x] + 1) + 3 * (c.delta[1][y] + 1) + 9 * (c.delta[2][zz] + 1);
-            v[j] = c.sbase[combo][x + N * (y + N * zz)];
+            const int k = x + N * (y + N * zz);
+            v[j] = c.sbase[combo][c.sflip[combo] ? mirror_k(k, x, y, zz, c.sflip[combo], N) : k];
           }
         } else {
 #pragma unroll
@@ -760,6 +765,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.fse = c.fsb + 2;
   c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
   c.sbase = reinterpret_cast<const double**>(smem + C::OFF_SBASE);
+  c.sflip = reinterpret_cast<int8_t*>(smem + C::OFF_SFLIP);
   int8_t (*sdelta)[kMaxN] = reinterpret_cast<int8_t (*)[kMaxN]>(smem + C::OFF_DELTA);
   load_delta(p.tp, sdelta);
   c.delta = sdelta;

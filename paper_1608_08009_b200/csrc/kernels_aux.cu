@@ -32,13 +32,16 @@ __global__ void __launch_bounds__(256) k_transport_cfl1(const double* __restrict
   constexpr int n = DV == 3 ? N * N * N : N * N;
   __shared__ int8_t sdelta[3][kMaxN];
   __shared__ const double* sbase[27];
+  __shared__ int8_t sflip[27];  // mirrored velocity components per source (specular reflection)
   load_delta(tp, sdelta);
   for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
     __syncthreads();  // sdelta loaded / the previous cell's sources no longer read
     if (threadIdx.x < 27) {
-      const int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1, (int)threadIdx.x / 9 - 1};
+      int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1, (int)threadIdx.x / 9 - 1};
       const bool is_solid = solid != nullptr && solid[cell];
-      sbase[threadIdx.x] = is_solid ? f_in + cell * n : source_base(f_in, tp, cell_coord(tp, cell), d, n);
+      int flip = 0;
+      sbase[threadIdx.x] = is_solid ? f_in + cell * n : source_resolve(f_in, tp, cell_coord(tp, cell), d, n, flip);
+      sflip[threadIdx.x] = (int8_t)flip;
     }
     __syncthreads();
     double* out = f_out + cell * n;
@@ -46,7 +49,8 @@ __global__ void __launch_bounds__(256) k_transport_cfl1(const double* __restrict
     for (int k = threadIdx.x; k < n; k += 256) {
       const int kx = k % N, ky = (k / N) % N, kz = DV == 3 ? k / (N * N) : 0;
       const int combo = (sdelta[0][kx] + 1) + 3 * (sdelta[1][ky] + 1) + 9 * (sdelta[2][kz] + 1);
-      out[k] = __ldg(sbase[combo] + k);
+      const int ks = sflip[combo] ? mirror_k(k, kx, ky, kz, sflip[combo], N) : k;
+      out[k] = __ldg(sbase[combo] + ks);
     }
   }
 }

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
   constexpr int NM = DV + 2;  // moments: 1, v (DV), |v|^2
   __shared__ int8_t sdelta[3][kMaxN];
   __shared__ const double* sbase[27];
+  __shared__ int8_t sflip[27];
   __shared__ double red[8][5];
   __shared__ double sexp[3][kMaxN];  // separable Maxwellian factors exp(-(v_k - u_a)^2 / (2T))
   load_delta(p.tp, sdelta);
@@ -63,8 +64,10 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
     const CellCoord cc = cell_coord(p.tp, cell);
     __syncthreads();  // sdelta loaded / previous cell's sources no longer read
     if (p.tp.dx > 0 && p.tp.cfl1 && threadIdx.x < 27) {
-      const int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1, (int)threadIdx.x / 9 - 1};
-      sbase[threadIdx.x] = source_base(p.f_in, p.tp, cc, d, n);
+      int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1, (int)threadIdx.x / 9 - 1};
+      int flip = 0;
+      sbase[threadIdx.x] = source_resolve(p.f_in, p.tp, cc, d, n, flip);
+      sflip[threadIdx.x] = (int8_t)flip;
     }
     __syncthreads();
     auto fstar = [&](int k) -> double {  // a1 + a3 for velocity k of this cell
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
       if (p.tp.dx == 0) return __ldg(p.f_in + cell * n + k);
       if (p.tp.cfl1) {
         const int combo = (sdelta[0][kx] + 1) + 3 * (sdelta[1][ky] + 1) + 9 * (sdelta[2][kz] + 1);
-        return sbase[combo][k];
+        return sbase[combo][sflip[combo] ? mirror_k(k, kx, ky, kz, sflip[combo], N) : k];
       }
       return gather_fstar(p.f_in, p.tp, cc, k, kx, ky, kz, n, sdelta);
     };

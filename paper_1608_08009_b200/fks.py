@@ -82,6 +82,10 @@ class Context:
         m = np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
         check(self._lib.fks_set_solid(self.handle, m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))), "fks_set_solid")
 
+    def set_specular(self, on=True):
+        """NEXT-1: specular reflection at solid cells (fks_set_specular)."""
+        check(self._lib.fks_set_specular(self.handle, int(bool(on))), "fks_set_specular")
+
     def set_stream(self, stream):
         """stream: a torch.cuda.Stream (or None for the default stream)."""
         check(self._lib.fks_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream if stream else 0)),

@@ -254,6 +254,83 @@ def test_collide_3d_one_group_many_cells(torch, fks, N, L, ncells, monkeypatch):
         assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
 
 
+# ---------------------------------------------------------------- NEXT-1: specular reflection
+def _solid_block(M, cells):
+    solid = np.zeros(tuple(M[::-1]), dtype=bool)
+    for c in cells:
+        solid[tuple(reversed(c))] = True
+    return solid
+
+
+@pytest.mark.parametrize("dxd,dv,M,N,bc,cells,cfl", [
+    (1, 3, [9], 8, [transport.PERIODIC] * 2, [(4,)], 0.93),
+    (2, 2, [6, 6], 16, [transport.PERIODIC] * 4, [(2, 2), (3, 2), (2, 3)], 0.93),
+    (2, 3, [6, 5], 8, [transport.GHOST, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC],
+     [(2, 1), (2, 2)], 0.93),
+    (3, 3, [4, 4, 3], 8, [transport.PERIODIC] * 6, [(1, 1, 1), (2, 1, 1), (1, 2, 1)], 0.93),
+    (2, 2, [7, 6], 8, [transport.PERIODIC] * 4, [(3, 3)], 1.8),    # CFL > 1: general gather
+])
+def test_transport_specular_bitwise(torch, fks, dxd, dv, M, N, bc, cells, cfl):
+    """fks_transport with specular reflection = the oracle's gather_specular, bitwise, 5 steps."""
+    L = 5.0
+    F, h, _, ghosts = _spatial_case(dxd, dv, M, N, L, bc, seed=13)
+    dt = cfl * h / (L - L / N)
+    solid = _solid_block(M, cells)
+    ctx = fks.Context(dv, dxd, M, N, L, 8 if dv == 2 else 24, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_solid(solid)
+    ctx.set_specular(True)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(5):
+        ctx.transport(a, b, dt)
+        a, b = b, a
+        ref = transport.gather_specular(ref, s, dxd, dv, N, L, dt, h, bc, ghosts, solid)
+    np.testing.assert_array_equal(host(a), ref)
+
+
+@pytest.mark.parametrize("model", ["boltzmann", "bgk"])
+def test_step_specular(torch, fks, model):
+    """Fused steps with specular reflection (3D kernel's per-cell source table with mirrored
+    components; BGK kernel) against the oracle's gather_specular followed by its collision."""
+    dxd, dv, M, N, L = 2, 3, [5, 4], 8, 6.0
+    bc = [transport.GHOST, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC]
+    F, h, dt, ghosts = _spatial_case(dxd, dv, M, N, L, bc, seed=17)
+    solid = _solid_block(M, [(2, 1), (2, 2)])
+    ctx = fks.Context(dv, dxd, M, N, L, 24, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_solid(solid)
+    ctx.set_specular(True)
+    ctx.set_params(tau=0.5)
+    tab = tables.build_tables(dv, N, L)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(2):
+        if model == "bgk":
+            ctx.step_bgk(a, b, dt, bgk.NU_RHO, 0.0)
+        else:
+            ctx.step(a, b, dt)
+        a, b = b, a
+        fstar = transport.gather_specular(ref, s, dxd, dv, N, L, dt, h, bc, ghosts, solid)
+        nxt = np.empty_like(ref)
+        for j in range(int(np.prod(M))):
+            idx = np.unravel_index(j, tuple(M[::-1]))
+            if solid[idx]:
+                nxt[idx] = ref[idx]
+            elif model == "bgk":
+                nxt[idx] = bgk.bgk_step_cell(fstar[idx], dt, 0.5, bgk.NU_RHO, 0.0, dv, N, L)
+            else:
+                Q = projection.project_zero_moments(collision.collide_fft(fstar[idx], tab), dv, N, L)
+                nxt[idx] = fstar[idx] + (dt / 0.5) * Q
+        ref = nxt
+    got = host(a).reshape((-1,) + (N,) * dv)
+    ref = ref.reshape((-1,) + (N,) * dv)
+    for i in range(ref.shape[0]):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
 # ---------------------------------------------------------------- NEXT-2: BGK step
 @pytest.mark.parametrize("dv,N,L,kind", [(2, 32, 9.0, "bkw"), (2, 16, 6.0, "random"), (3, 16, 7.0, "smooth"),
                                          (3, 32, 7.0, "random")])
