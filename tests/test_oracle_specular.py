@@ -83,3 +83,16 @@ def test_single_particle_reflects_off_a_wall():
     assert delta[kx] == -1                 # the source of +v_x is the cell below: this one moves up
     G = transport.gather_specular(F, 0, dxd, dv, N, L, dt, dx, [transport.PERIODIC] * 2, None, solid)
     assert G[3, ky, N - 1 - kx] == 1.0 and np.sum(G) == 1.0
+
+
+def test_reentry_inflow_schedule():
+    """eq. BCs: the printed branches, |u_BC| = 3 throughout, continuity at t1, t2."""
+    f = workloads.reentry_inflow_velocity
+    t1, t2 = 1.5, 3 * np.sqrt(2) / 2 + 1.5
+    assert f(1.0) == (3.0, 0.0)
+    assert np.allclose(f(t2 + 0.5), (3 * np.sqrt(2) / 2, 3 * np.sqrt(2) / 2), rtol=0, atol=1e-15)
+    assert np.allclose(f(t1 + 1.0), (2 * np.sqrt(2), 1.0), rtol=0, atol=1e-15)
+    for t in np.linspace(0, 10, 101):
+        assert abs(np.hypot(*f(t)) - 3.0) < 1e-14
+    for tj in (t1, t2):
+        assert np.allclose(f(tj - 1e-12), f(tj + 1e-12), atol=1e-9)

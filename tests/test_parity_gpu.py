@@ -331,6 +331,43 @@ def test_step_specular(torch, fks, model):
         assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
 
 
+def test_reentry_inflow_schedule_with_specular_solids(torch, fks):
+    """NEXT-1 together: the time-dependent inflow of eq. BCs through fks_set_ghost every step and
+    specular reflection at a solid box, fused steps vs the oracle with the same ghosts per step."""
+    dxd, dv, M, N, L = 2, 3, [6, 5], 8, 6.0
+    bc = [transport.GHOST, transport.OUTFLOW, transport.OUTFLOW, transport.OUTFLOW]
+    F, h, dt, _ = _spatial_case(dxd, dv, M, N, L, bc, seed=23)
+    c = dict(dv=dv, N=N, L=L)
+    solid = _solid_block(M, [(3, 2)])
+    ctx = fks.Context(dv, dxd, M, N, L, 24, h=h, bc=bc)
+    ctx.set_solid(solid)
+    ctx.set_specular(True)
+    ctx.set_params(tau=0.5)
+    tab = tables.build_tables(dv, N, L)
+    t0 = 1.5 - dt                                   # the inflow starts turning during the run
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(3):
+        g = workloads.reentry_inflow_ghost(c, t0 + s * dt)
+        ctx.set_ghost(0, dev(torch, g))
+        ctx.step(a, b, dt)
+        a, b = b, a
+        fstar = transport.gather_specular(ref, s, dxd, dv, N, L, dt, h, bc, {0: g}, solid)
+        nxt = np.empty_like(ref)
+        for j in range(int(np.prod(M))):
+            idx = np.unravel_index(j, tuple(M[::-1]))
+            if solid[idx]:
+                nxt[idx] = ref[idx]
+            else:
+                Q = projection.project_zero_moments(collision.collide_fft(fstar[idx], tab), dv, N, L)
+                nxt[idx] = fstar[idx] + (dt / 0.5) * Q
+        ref = nxt
+    got = host(a).reshape((-1,) + (N,) * dv)
+    ref = ref.reshape((-1,) + (N,) * dv)
+    for i in range(ref.shape[0]):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
 # ---------------------------------------------------------------- NEXT-2: BGK step
 @pytest.mark.parametrize("dv,N,L,kind", [(2, 32, 9.0, "bkw"), (2, 16, 6.0, "random"), (3, 16, 7.0, "smooth"),
                                          (3, 32, 7.0, "random")])

@@ -5,4 +5,5 @@ transport or collision): it only evaluates the paper's initial/boundary profiles
 velocity nodes and draws seeded random numbers.  Both the CUDA path and the oracle consume
 its bytes; neither imports the other.
 """
-from .gen import CONFIGS, config, initial_state, family, ghost_vectors, solid_mask  # noqa: F401
+from .gen import (CONFIGS, config, initial_state, family, ghost_vectors, solid_mask,  # noqa: F401
+                  reentry_inflow_velocity, reentry_inflow_ghost)

@@ -123,6 +123,28 @@ def ghost_vectors(c):
     return {}
 
 
+def reentry_inflow_velocity(t):
+    """(u_x, u_y)_BC(t) of eq. BCs: (3, 0) up to t1 = 3/2, then (sqrt(9 - g^2), g) with
+    g = t - t1 up to t2 = 3 sqrt(2)/2 + t1, then (3 sqrt(2)/2, 3 sqrt(2)/2): a speed-3 inflow turning
+    by 45 degrees (NEXT-1 "time-dependent inflow schedule")."""
+    t1 = 1.5
+    t2 = 3.0 * np.sqrt(2.0) / 2.0 + t1
+    if t <= t1:
+        return (3.0, 0.0)
+    if t <= t2:
+        g = t - t1
+        return (float(np.sqrt(9.0 - g * g)), float(g))
+    return (3.0 * np.sqrt(2.0) / 2.0, 3.0 * np.sqrt(2.0) / 2.0)
+
+
+def reentry_inflow_ghost(c, t):
+    """The west-face inflow ghost vector of C4 at time t: Maxwellian (rho, T) = (1, 1) with the
+    velocity of eq. BCs (boundary data, pointwise like the initial data)."""
+    dv, N, L = c["dv"], c["N"], c["L"]
+    ux, uy = reentry_inflow_velocity(t)
+    return maxwellian(_vgrid(dv, N, L), 1.0, (ux, uy, 0.0)[:dv], 1.0)
+
+
 def solid_mask(c):
     """Boolean [cells...] of solid cells (cell centre inside an obstacle), or None."""
     if c["name"] == "C4":
