@@ -22,24 +22,26 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(s, verbose):
+    src = os.path.join(CSRC, s)
+    obj = os.path.join(CSRC, s.replace(".cu", ".o"))
+    r = subprocess.run([NVCC, *FLAGS, "-c", src, "-o", obj], capture_output=True, text=True)
+    if verbose or r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {s}")
+    with open(os.path.join(CSRC, s.replace(".cu", ".ptxas.txt")), "w") as fh:
+        fh.write(r.stderr)
+    return obj
+
+
 def build(force=False, verbose=False):
-    """Compile every .cu to an object, link libfks.so; returns the library path."""
+    """Compile every .cu to an object (in parallel), link libfks.so; returns the library path."""
     if not force and not _stale():
         return LIB
-    objs = []
-    for s in SOURCES:
-        src = os.path.join(CSRC, s)
-        obj = os.path.join(CSRC, s.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if verbose or r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {s}")
-        log = os.path.join(CSRC, s.replace(".cu", ".ptxas.txt"))
-        with open(log, "w") as fh:
-            fh.write(r.stderr)
-        objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
