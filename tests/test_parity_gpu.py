@@ -449,6 +449,27 @@ def test_nonfinite_flag(torch, fks):
     ctx.check()  # flag cleared
 
 
+def test_next_entry_points_argument_errors(torch, fks):
+    """fks_step_bgk / fks_set_specular reject bad arguments synchronously (include/fks.h)."""
+    N, L = 8, 7.0
+    f = workloads.family("smooth", 3, N, L, 2, seed=6)
+    ctx = fks.Context(3, 0, [2], N, L, 24)
+    out = torch.empty(2, N, N, N, dtype=torch.float64, device="cuda")
+    for rule, mu in ((7, 0.0), (bgk.NU_CONST, 0.0), (bgk.NU_CONST, -1.0)):
+        with pytest.raises(fks.FksError) as ei:
+            ctx.step_bgk(dev(torch, f), out, 0.01, rule, mu)
+        assert ei.value.status == -1  # FKS_E_INVAL
+    a = dev(torch, f)
+    with pytest.raises(fks.FksError):
+        ctx.step_bgk(a, a, 0.01, bgk.NU_RHO, 0.0)  # in place is not allowed
+    # specular reflection is refused on a partitioned grid (HALO faces)
+    ctx2 = fks.Context(3, 1, [4], N, L, 24, h=0.1, bc=[fks.BC_HALO, fks.BC_OUTFLOW])
+    with pytest.raises(fks.FksError) as ei:
+        ctx2.set_specular(True)
+    assert ei.value.status == -2  # FKS_E_UNSUPPORTED
+    ctx2.set_specular(False)
+
+
 def test_deterministic_and_host_path(torch, fks):
     """Two runs are bitwise identical; fks_step_host (host buffers) equals the device path."""
     c = workloads.config("C2")
