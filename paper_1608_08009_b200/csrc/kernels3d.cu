@@ -57,7 +57,7 @@ struct Cfg3 {
   static constexpr int WPLANE = N * N;        // plane in the exchange buffer
   static constexpr size_t WBUF = (size_t)N * WPLANE;  // one exchange buffer (all N j_z planes)
 #ifndef FKS_NBUF
-#define FKS_NBUF 6  // 4: 19.4 ms, 6: 19.15 ms, 8: 20.3 ms (L2 footprint) on C2
+#define FKS_NBUF 5  // C2: 4 slots 19.39 ms / 552 KB DRAM per cell, 5: 19.17 / 724 KB, 6: 19.16 / 2.5 MB (the ring spills), 8: 20.3 ms
 #endif
   static constexpr int NBUF = FKS_NBUF;  // exchange ring slots: the z group runs up to NBUF-1 items ahead
   static constexpr int FHAT_COLS = 4 * N;     // one f^ pencil (N complex fp64) per lane (z group)
