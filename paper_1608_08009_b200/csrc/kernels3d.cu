@@ -78,7 +78,7 @@ struct Cfg3 {
   static constexpr int TGW = NW >= 2 ? 2 : 1;          // warps per table group
   static constexpr int NTG = NW / TGW;                 // table groups
   // mbarriers: tbar[2][NTG], wbar[2][NW], fsb[2] (f* cache written), fse[2] (f* cache read)
-  static constexpr int NMBAR = 2 * NTG + 2 * NW + 4;
+  static constexpr int NMBAR = 2 * NTG + 2 * NW + 4 + 2 * NTG;  // ... + tempty[2][NTG]
   static constexpr size_t OFF_MBAR = OFF_PLN + 2 * (size_t)PSLAB * 16;
   static constexpr size_t OFF_TMEM = OFF_MBAR + 8 * NMBAR;
   static constexpr size_t OFF_PART = OFF_TMEM + 8;           // lambda[5] + warp partials [4][5]
@@ -307,6 +307,7 @@ struct Ctx3 {
   uint64_t* wbar;  // [2][NW] plane(s) of a warp landed
   uint64_t* fsb;   // [2] f* cache of parity b written (z group, GT arrivals)
   uint64_t* fse;   // [2] f* cache of parity b read for the last time (xy group, GT arrivals)
+  uint64_t* tempty;  // [2][NTG] table buffer b of a table group read by its warps (TGW arrivals)
   double* part;    // [8] epilogue scratch (moment sums, lambda)
   const int8_t (*delta)[kMaxN];  // shift table (SMEM copy)
   const double** sbase;          // [27] per-cell transport sources (forward gather, dx > 0)
@@ -350,11 +351,8 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
     bulk_load(c.tbuf + (j & 1) * TB + (size_t)trow0 * N, tab_rank + (size_t)j * P * C::SLAB + (size_t)trow0 * N,
               (uint32_t)(trow1 - trow0) * N * 16, c.tbar + (j & 1) * NTG + tgi);
   };
-  auto group_sync = [&]() {  // the warps of this table group
-    if constexpr (TGW == 2) named_bar(3 + tgi, 64);
-    else __syncwarp();
-  };
   uint32_t tphase = 0;  // bit b: parity of this group's table buffer b
+  uint32_t tephase = 0;  // bit b: parity of tempty of this group's buffer b
   unsigned pub = 0;     // this warp's first z item not yet published
   unsigned seq = 0;     // exchange-buffer sequence index of the next item
   unsigned ncell = 0;   // cells done by this group
@@ -520,8 +518,18 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
       TSTAMP(2048 + j * 8 + 1);
       zpass_compute<N, P>(taddr, c.tbuf + tb * TB, tx, tm, x);
       TSTAMP(2048 + j * 8 + 2);
-      group_sync();  // this group's table buffer tb consumed; the warp's z(j-1) stores precede this
-      if (tg_leader && j + 2 < D) load_tab(j + 2);  // into the buffer just freed
+      __syncwarp();  // the warp's reads of table buffer tb and its z(j-1) stores precede this
+      if constexpr (TGW == 2) {
+        // the partner warp only announces it is done; the loading lane waits for it (mbarrier)
+        if (lane == 0) mbar_arrive(c.tempty + tb * NTG + tgi);
+        if (tg_leader && j + 2 < D) {
+          mbar_wait(c.tempty + tb * NTG + tgi, (tephase >> tb) & 1u);
+          load_tab(j + 2);  // into the buffer just freed
+        }
+        tephase ^= 1u << tb;
+      } else {
+        if (tg_leader && j + 2 < D) load_tab(j + 2);  // into the buffer just freed
+      }
       if (lane == 0) {
         if (use > 0) sync_wait_free(&gs->cons[slot], WP * use, cons_seen);
         // Publish this warp's z items in batches of FKS_PUB: one release fence (which waits for the
@@ -763,6 +771,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.wbar = c.tbar + 2 * C::NTG;
   c.fsb = c.wbar + 2 * C::NW;
   c.fse = c.fsb + 2;
+  c.tempty = c.fse + 2;
   c.part = reinterpret_cast<double*>(smem + C::OFF_PART);
   c.sbase = reinterpret_cast<const double**>(smem + C::OFF_SBASE);
   c.sflip = reinterpret_cast<int8_t*>(smem + C::OFF_SFLIP);
@@ -792,6 +801,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
     for (int i = 0; i < 2; ++i) {
       mbar_init(c.fsb + i, C::GT);
       mbar_init(c.fse + i, C::GT);
+      for (int g = 0; g < C::NTG; ++g) mbar_init(c.tempty + i * C::NTG + g, C::TGW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
