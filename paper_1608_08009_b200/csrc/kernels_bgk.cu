@@ -3,12 +3,14 @@
 // E[U] = E~ + Phi^T (Phi Phi^T)^{-1} (Phi f - Phi E~); P:909 the 1/tau rescaling
 // forward Euler; nu = rho or a constant mu; the Euler limit returns E.
 //
-// One CTA per cell (persistent): pass 1 gathers f* and reduces its 5 (2D: 4) moments, pass 2
-// evaluates the pointwise Maxwellian and reduces its moments, pass 3 writes
+// One CTA per cell (persistent): pass 1 gathers f* and reduces its 5 (2D: 4) moments, the
+// Maxwellian's moments come from 1D sums (it is separable, O(DV N) work), pass 3 writes
 // f* + (dt/tau) nu (E - f*).  f* is re-gathered (an L2 hit) instead of held: a 32^3 cell is
 // 256 KiB.  Reductions are fixed-order (warp shuffles, then warps in order): deterministic.
 // HBM-bound: 16 B per phase-space update (read f, write f); the Maxwellian is separable, so a
 // cell needs only DV * N exponentials.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -25,7 +27,8 @@ __device__ __forceinline__ void phi_row(int k, double L, double h, double (&ph)[
   ph[4] = vx * vx + vy * vy + vz * vz;
 }
 
-// Fixed-order block sum of m[0..4] (256 threads); every thread gets the totals.
+// Fixed-order block sum of m[0..4] (NT threads); every thread gets the totals.
+template <int NT>
 __device__ __forceinline__ void block_sum5(double (&m)[5], double (*red)[5]) {
 #pragma unroll
   for (int c = 0; c < 5; ++c) {
@@ -41,19 +44,21 @@ __device__ __forceinline__ void block_sum5(double (&m)[5], double (*red)[5]) {
 #pragma unroll
   for (int c = 0; c < 5; ++c) {
     double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += red[w][c];
+    for (int w = 0; w < NT / 32; ++w) s += red[w][c];
     m[c] = s;
   }
 }
 
-template <int N, int DV>
-__global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
+// NT threads per CTA.  The CTA count is chosen so that the cells in flight (one per CTA, plus the
+// prefetched next one) stay L2-resident between pass 1 and pass 3 (see launch_bgk).
+template <int N, int DV, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bgk(const BgkParams p, const int prefetch) {
   constexpr int n = DV == 3 ? N * N * N : N * N;
   constexpr int NM = DV + 2;  // moments: 1, v (DV), |v|^2
   __shared__ int8_t sdelta[3][kMaxN];
   __shared__ const double* sbase[27];
   __shared__ int8_t sflip[27];
-  __shared__ double red[8][5];
+  __shared__ double red[NT / 32][5];
   __shared__ double sexp[3][kMaxN];  // separable Maxwellian factors exp(-(v_k - u_a)^2 / (2T))
   load_delta(p.tp, sdelta);
   const double h = p.dv;
@@ -80,7 +85,7 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
       return gather_fstar(p.f_in, p.tp, cc, k, kx, ky, kz, n, sdelta);
     };
     // the next cell of this CTA (homogeneous case: contiguous) -> L2 while this one is processed
-    if (p.tp.dx == 0 && threadIdx.x == 0 && !p.cell_list && it + gridDim.x < p.ncells)
+    if (prefetch && p.tp.dx == 0 && threadIdx.x == 0 && !p.cell_list && it + gridDim.x < p.ncells)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.f_in + (int64_t)(it + gridDim.x) * n),
                    "r"((uint32_t)(n * sizeof(double)))
                    : "memory");
@@ -88,7 +93,8 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
     double m[5] = {0, 0, 0, 0, 0};
     if (p.tp.dx == 0) {
       const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * n);
-      for (int k2 = threadIdx.x; k2 < n / 2; k2 += 256) {
+#pragma unroll 4
+      for (int k2 = threadIdx.x; k2 < n / 2; k2 += NT) {
         const double2 f2 = __ldg(src + k2);
         double ph[5], pq[5];
         phi_row<N, DV>(2 * k2, p.L, h, ph);
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
         for (int c = 0; c < 5; ++c) m[c] = fma(pq[c], f2.y, fma(ph[c], f2.x, m[c]));
       }
     } else {
-      for (int k = threadIdx.x; k < n; k += 256) {
+      for (int k = threadIdx.x; k < n; k += NT) {
         const double f = fstar(k);
         double ph[5];
         phi_row<N, DV>(k, p.L, h, ph);
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
         for (int c = 0; c < 5; ++c) m[c] = fma(ph[c], f, m[c]);
       }
     }
-    block_sum5(m, red);
+    block_sum5<NT>(m, red);
     double U[5];  // Phi f* in the row order 1, v_x .. v_{DV-1}, |v|^2
     U[0] = m[0];
     for (int a = 0; a < DV; ++a) U[1 + a] = m[1 + a];
@@ -129,16 +135,28 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
       const double e = amp * sexp[0][k % N] * sexp[1][(k / N) % N];
       return DV == 3 ? e * sexp[2][k / (N * N)] : e;
     };
-    // pass 2: moments of E~, then lambda = (Phi Phi^T)^{-1} (Phi f* - Phi E~)
-    double me[5] = {0, 0, 0, 0, 0};
-    for (int k = threadIdx.x; k < n; k += 256) {
-      const double e = maxw(k);
-      double ph[5];
-      phi_row<N, DV>(k, p.L, h, ph);
-#pragma unroll
-      for (int c = 0; c < 5; ++c) me[c] = fma(ph[c], e, me[c]);
+    // pass 2: moments of E~, then lambda = (Phi Phi^T)^{-1} (Phi f* - Phi E~).  E~ and every row of
+    // Phi are separable on the tensor velocity grid, so Sum_k E~(k) Phi(k) is a product of 1D sums
+    // S0_a = Sum e_a, S1_a = Sum v e_a, S2_a = Sum v^2 e_a (the same finite sum, reordered).
+    double S0[3] = {1, 1, 1}, S1[3] = {0, 0, 0}, S2[3] = {0, 0, 0};
+    for (int a = 0; a < DV; ++a) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int k = 0; k < N; ++k) {
+        const double e = sexp[a][k], v = node_v(k, p.L, h);
+        s0 += e;
+        s1 = fma(v, e, s1);
+        s2 = fma(v * v, e, s2);
+      }
+      S0[a] = s0;
+      S1[a] = s1;
+      S2[a] = s2;
     }
-    block_sum5(me, red);
+    double me[5];
+    me[0] = amp * S0[0] * S0[1] * S0[2];
+    me[1] = amp * S1[0] * S0[1] * S0[2];
+    me[2] = amp * S0[0] * S1[1] * S0[2];
+    me[3] = amp * S0[0] * S0[1] * S1[2];
+    me[4] = amp * (S2[0] * S0[1] * S0[2] + S0[0] * S2[1] * S0[2] + (DV == 3 ? S0[0] * S0[1] * S2[2] : 0.0));
     double r[5];
     r[0] = U[0] - me[0];
     for (int a = 0; a < DV; ++a) r[1 + a] = U[1 + a] - me[1 + a];
@@ -167,13 +185,14 @@ __global__ void __launch_bounds__(256) k_bgk(const BgkParams p) {
     if (p.tp.dx == 0) {
       const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * n);
       double2* dst = reinterpret_cast<double2*>(out);
-      for (int k2 = threadIdx.x; k2 < n / 2; k2 += 256) {
+#pragma unroll 4
+      for (int k2 = threadIdx.x; k2 < n / 2; k2 += NT) {
         const double2 f2 = __ldg(src + k2);
         const double o0 = update(2 * k2, f2.x), o1 = update(2 * k2 + 1, f2.y);
         dst[k2] = make_double2(o0, o1);
       }
     } else {
-      for (int k = threadIdx.x; k < n; k += 256) out[k] = update(k, fstar(k));
+      for (int k = threadIdx.x; k < n; k += NT) out[k] = update(k, fstar(k));
     }
     if (bad) atomicOr(p.nonfinite, 1);
   }
@@ -216,19 +235,22 @@ __global__ void __launch_bounds__(256) k_bgk2w(const BgkParams p) {
     }
     __syncwarp();
     auto maxw = [&](int k) { return amp * sexp[wv][0][k % N] * sexp[wv][1][k / N]; };
-    double me[5] = {0, 0, 0, 0, 0};
-    for (int k = lane; k < n; k += 32) {
-      const double e = maxw(k);
-      double ph[5];
-      phi_row<N, 2>(k, p.L, h, ph);
-#pragma unroll
-      for (int c = 0; c < 5; ++c) me[c] = fma(ph[c], e, me[c]);
+    // separable moments of E~ (as in k_bgk)
+    double S0[2], S1[2], S2[2];
+    for (int a = 0; a < 2; ++a) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int k = 0; k < N; ++k) {
+        const double e = sexp[wv][a][k], v = node_v(k, p.L, h);
+        s0 += e;
+        s1 = fma(v, e, s1);
+        s2 = fma(v * v, e, s2);
+      }
+      S0[a] = s0;
+      S1[a] = s1;
+      S2[a] = s2;
     }
-#pragma unroll
-    for (int c = 0; c < 5; ++c) {
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) me[c] += __shfl_xor_sync(0xffffffffu, me[c], o);
-    }
+    const double me[5] = {amp * S0[0] * S0[1], amp * S1[0] * S0[1], amp * S0[0] * S1[1], 0.0,
+                          amp * (S2[0] * S0[1] + S0[0] * S2[1])};
     const double r[4] = {m[0] - me[0], m[1] - me[1], m[2] - me[2], m[4] - me[4]};
     double lam[4];
 #pragma unroll
@@ -269,9 +291,23 @@ cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStre
     if (N == 16) { k_bgk2w<16><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
     if (N == 32) { k_bgk2w<32><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
   }
-  const unsigned nb = (unsigned)(p.ncells < sm_count * 8 ? p.ncells : sm_count * 8);
-#define FKS_BGK(NN, DD) \
-  if (N == NN && dv == DD) { k_bgk<NN, DD><<<nb, 256, 0, s>>>(p); return cudaGetLastError(); }
+  // 3D cells are 256 KiB: CTAs per SM x 148 x 256 KiB (x2 with the next-cell prefetch) must fit
+  // the 126 MB L2, or pass 3 re-reads f from HBM.  FKS_BGK_CFG (experiment knob) = 0: 256 threads x
+  // 8 CTAs/SM + prefetch (the round-1 launch); 2: 512 x 2, no prefetch; 3: 512 x 1 + prefetch;
+  // 4: 512 x 2 capped at 64 registers (2 resident), no prefetch; 5: 256 x 4 at 64 registers.
+  int cfg = (dv == 3 && N == 32) ? 4 : 0;
+  if (const char* e = getenv("FKS_BGK_CFG")) cfg = atoi(e);
+  const int per_sm = cfg == 0 ? 8 : (cfg == 2 || cfg == 4) ? 2 : cfg == 5 ? 4 : 1;
+  const int pf = (cfg == 0 || cfg == 3) ? 1 : 0;
+  const unsigned nb = (unsigned)(p.ncells < sm_count * per_sm ? p.ncells : sm_count * per_sm);
+#define FKS_BGK(NN, DD)                                                                      \
+  if (N == NN && dv == DD) {                                                                 \
+    if (cfg == 4) k_bgk<NN, DD, 512, 2><<<nb, 512, 0, s>>>(p, pf);                           \
+    else if (cfg == 5) k_bgk<NN, DD, 256, 4><<<nb, 256, 0, s>>>(p, pf);                      \
+    else if (cfg == 2 || cfg == 3) k_bgk<NN, DD, 512, 1><<<nb, 512, 0, s>>>(p, pf);           \
+    else k_bgk<NN, DD, 256, 1><<<nb, 256, 0, s>>>(p, pf);                                    \
+    return cudaGetLastError();                                                               \
+  }
   FKS_BGK(8, 2) FKS_BGK(16, 2) FKS_BGK(32, 2) FKS_BGK(8, 3) FKS_BGK(16, 3) FKS_BGK(32, 3)
 #undef FKS_BGK
   return cudaErrorInvalidValue;
