@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(NT, MINB) k_bgk(const BgkParams p, const int p
 
 // 2D cells (N^2 <= 1024 nodes): one warp per cell, homogeneous (dx = 0) only; reductions are
 // warp shuffles in a fixed order.  Same arithmetic as k_bgk.
-template <int N>
-__global__ void __launch_bounds__(256) k_bgk2w(const BgkParams p) {
+template <int N, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_bgk2w(const BgkParams p) {
   constexpr int n = N * N;
   __shared__ double sexp[8][2][N];
   const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(256) k_bgk2w(const BgkParams p) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
     const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * n);
     double m[5] = {0, 0, 0, 0, 0};
+#pragma unroll 4
     for (int k2 = lane; k2 < n / 2; k2 += 32) {
       const double2 f2 = __ldg(src + k2);
       double ph[5], pq[5];
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(256) k_bgk2w(const BgkParams p) {
       return o;
     };
     double2* dst = reinterpret_cast<double2*>(p.f_out + cell * n);
+#pragma unroll 4
     for (int k2 = lane; k2 < n / 2; k2 += 32) {
       const double2 f2 = __ldg(src + k2);
       const double o0 = update(2 * k2, f2.x), o1 = update(2 * k2 + 1, f2.y);
@@ -286,10 +288,21 @@ __global__ void __launch_bounds__(256) k_bgk2w(const BgkParams p) {
 cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStream_t s) {
   if (p.ncells == 0) return cudaSuccess;
   if (dv == 2 && p.tp.dx == 0) {
-    const unsigned nw = (unsigned)((p.ncells + 7) / 8 < sm_count * 8 ? (p.ncells + 7) / 8 : sm_count * 8);
-    if (N == 8) { k_bgk2w<8><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
-    if (N == 16) { k_bgk2w<16><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
-    if (N == 32) { k_bgk2w<32><<<nw, 256, 0, s>>>(p); return cudaGetLastError(); }
+    // FKS_BGK2_CFG (experiment knob): resident CTAs per SM the register cap aims at (1, 3 or 4);
+    // 3 (80 registers) measured best at the C1 shape (profiles/r01_optimisation_log.md)
+    int minb = 3;
+    if (const char* e = getenv("FKS_BGK2_CFG")) minb = atoi(e);
+    const int per_sm = minb == 1 ? 8 : 2 * minb;
+    const unsigned nw = (unsigned)((p.ncells + 7) / 8 < sm_count * per_sm ? (p.ncells + 7) / 8 : sm_count * per_sm);
+#define FKS_BGK2(NN)                                                        \
+    if (N == NN) {                                                          \
+      if (minb == 4) k_bgk2w<NN, 4><<<nw, 256, 0, s>>>(p);                  \
+      else if (minb == 3) k_bgk2w<NN, 3><<<nw, 256, 0, s>>>(p);             \
+      else k_bgk2w<NN, 1><<<nw, 256, 0, s>>>(p);                            \
+      return cudaGetLastError();                                            \
+    }
+    FKS_BGK2(8) FKS_BGK2(16) FKS_BGK2(32)
+#undef FKS_BGK2
   }
   // 3D cells are 256 KiB: CTAs per SM x 148 x 256 KiB (x2 with the next-cell prefetch) must fit
   // the 126 MB L2, or pass 3 re-reads f from HBM.  FKS_BGK_CFG (experiment knob) = 0: 256 threads x
