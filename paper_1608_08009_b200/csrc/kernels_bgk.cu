@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(NT, MINB) k_bgk(const BgkParams p, const int p
         for (int c = 0; c < 5; ++c) m[c] = fma(pq[c], f2.y, fma(ph[c], f2.x, m[c]));
       }
     } else {
+#pragma unroll 4
       for (int k = threadIdx.x; k < n; k += NT) {
         const double f = fstar(k);
         double ph[5];
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(NT, MINB) k_bgk(const BgkParams p, const int p
         dst[k2] = make_double2(o0, o1);
       }
     } else {
+#pragma unroll 4
       for (int k = threadIdx.x; k < n; k += NT) out[k] = update(k, fstar(k));
     }
     if (bad) atomicOr(p.nonfinite, 1);
