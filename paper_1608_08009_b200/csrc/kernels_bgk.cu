@@ -193,8 +193,10 @@ __global__ void __launch_bounds__(NT, MINB) k_bgk(const BgkParams p, const int p
         dst[k2] = make_double2(o0, o1);
       }
     } else {
+      // with transport, pass 3 walks the cell backwards: the neighbour lines pass 1 gathered last
+      // are the likeliest L2 hits (C4 shape 3.43 -> 3.27 ms; homogeneous cells: slower, forward)
 #pragma unroll 4
-      for (int k = threadIdx.x; k < n; k += NT) out[k] = update(k, fstar(k));
+      for (int k = n - 1 - threadIdx.x; k >= 0; k -= NT) out[k] = update(k, fstar(k));
     }
     if (bad) atomicOr(p.nonfinite, 1);
   }
