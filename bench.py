@@ -324,12 +324,14 @@ def main():
         if c["dx_dim"] > 0:
             for face, g in workloads.ghost_vectors(c).items():
                 ctxb.set_ghost(face, torch.from_numpy(g).cuda())
+            if sl is not None:
+                ctxb.set_solid(sl)
         ctxb.set_params(tau=c["tau"])
         ctxb.set_stream(stream)
         ms_b = timed(lambda: ctxb.step_bgk(fa, fb, dt, fks.NU_RHO, 0.0), reps)
         ctxb.check()
-        gbs = 2 * ncells * n * 8 / (ms_b * 1e-3) / 1e9
-        extra["bgk_step"] = {"value": ncells / (ms_b * 1e-3), "unit": "cells/s", "ms": ms_b, "hbm_gbs": gbs,
+        gbs = 2 * nfluid_local * n * 8 / (ms_b * 1e-3) / 1e9
+        extra["bgk_step"] = {"value": nfluid_local / (ms_b * 1e-3), "unit": "cells/s", "ms": ms_b, "hbm_gbs": gbs,
                              "hbm_frac": gbs / hbm_peak(),
                              "what": "NEXT-2 fks_step_bgk (transport + conservative Maxwellian + Euler, nu = rho)"}
         ctxb.close()

@@ -86,7 +86,7 @@ def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None, cells=None):
     return out if sub is None else sub
 
 
-def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid):
+def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid, cells=None):
     """NEXT-1: f* with specular reflection at solid cells ("reflective boundary conditions",
     S:430-438 apply_solid_reflection; reading #23 of DESIGN.md).
 
@@ -100,21 +100,25 @@ def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid):
       otherwise c moves to it.
     The value is then read as in gather() from the source j + (the shifts of the axes that were not
     reflected), with the face rules (GHOST / OUTFLOW / PERIODIC), at the mirrored index k'.  Without
-    solids this is exactly gather().  Solid cells keep their values.  Plain scalar loops."""
+    solids this is exactly gather().  Solid cells keep their values.  Plain scalar loops.
+    cells: optional flat cell indices; then only those cells are computed and returned as
+    [len(cells), (N,)*dv] (F may then be any object with .shape and integer-tuple indexing)."""
     sp_shape = F.shape[:dxd]
     M = sp_shape[::-1]
     delta = shift_delta(n, N, L, dt, dx)
-    out = np.empty_like(F)
+    out = np.empty_like(F) if cells is None else np.empty((len(cells),) + (N,) * dv)
 
     def in_domain_solid(cell):                               # cell: list of dxd coordinates
         if any(c < 0 or c >= M[a] for a, c in enumerate(cell)):
             return False
         return bool(solid[tuple(cell[dxd - 1 - b] for b in range(dxd))])
 
-    for jflat in range(int(np.prod(sp_shape))):
+    todo = range(int(np.prod(sp_shape))) if cells is None else list(cells)
+    for pos, jflat in enumerate(todo):
         jidx = np.unravel_index(jflat, sp_shape)
+        oidx = jidx if cells is None else (pos,)
         if solid[jidx]:
-            out[jidx] = F[jidx]
+            out[oidx] = F[jidx]
             continue
         j = [jidx[dxd - 1 - a] for a in range(dxd)]
         for kidx in np.ndindex(*((N,) * dv)):
@@ -153,5 +157,5 @@ def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid):
                 val = ghosts[gface][kpidx]
             else:
                 val = F[tuple(s[dxd - 1 - b] for b in range(dxd)) + kpidx]
-            out[jidx + kidx] = val
+            out[oidx + kidx] = val
     return out

@@ -99,11 +99,11 @@ __device__ __forceinline__ const double* source_base(const double* __restrict__ 
       int s = cc.j[a] + d[a];
       if (s < 0) {
         const int b = tp.bc[2 * a];
-        if (b == 0) s += Ma;
+        if (b == 0) { s %= Ma; if (s < 0) s += Ma; }  // true modulo: |d| may exceed M_a (CFL > 1)
         else { if ((b == 1 || b == 3) && gface < 0) { gface = 2 * a; hplane = src; } s = 0; }
       } else if (s >= Ma) {
         const int b = tp.bc[2 * a + 1];
-        if (b == 0) s -= Ma;
+        if (b == 0) s %= Ma;
         else { if ((b == 1 || b == 3) && gface < 0) { gface = 2 * a + 1; hplane = src; } s = Ma - 1; }
       }
       src += s * stride;
@@ -130,9 +130,17 @@ __device__ __forceinline__ const double* source_resolve(const double* __restrict
     for (int a = 2; a >= 0; --a) {
       if (a >= tp.dx || d[a] == 0) continue;
       int nb = c[a] + d[a];
-      if (tp.bc[d[a] < 0 ? 2 * a : 2 * a + 1] == 0) nb = (nb + tp.M[a]) % tp.M[a];  // PERIODIC
+      if (tp.bc[d[a] < 0 ? 2 * a : 2 * a + 1] == 0) {  // PERIODIC: true modulo (|d| may exceed M_a)
+        nb %= tp.M[a];
+        if (nb < 0) nb += tp.M[a];
+      }
+      // the candidate origin is a solid cell only if EVERY coordinate is inside the domain (an
+      // axis undone earlier may have left c[b] outside through an OUTFLOW / GHOST / HALO face)
+      bool inside = nb >= 0 && nb < tp.M[a];
+      for (int b = 0; b < tp.dx; ++b)
+        if (b != a) inside &= c[b] >= 0 && c[b] < tp.M[b];
       bool is_solid = false;
-      if (nb >= 0 && nb < tp.M[a]) {
+      if (inside) {
         int64_t idx = 0, stride = 1;
         for (int b = 0; b < tp.dx; ++b) {
           idx += (int64_t)(b == a ? nb : c[b]) * stride;

@@ -322,7 +322,10 @@ fks_status set_cell_lists(fks_ctx* c, const uint8_t* solid_host) {
   return cuda_fail(cudaGetLastError());
 }
 
-void fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift) {
+// Returns FKS_E_UNSUPPORTED when a shift along the slab axis exceeds one cell while that axis has a
+// HALO face: the neighbour rank sends exactly one plane (halo width 1 at CFL <= 1, reading #15), so a
+// source two planes away would silently read the wrong plane.
+fks_status fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift) {
   std::memset(tp, 0, sizeof(*tp));
   tp->dx = with_shift ? c->grid.dx : 0;
   for (int a = 0; a < 3; ++a) tp->M[a] = (int)c->grid.M[a];
@@ -337,6 +340,13 @@ void fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift)
   tp->cfl1 = 1;
   for (int a = 0; a < 3; ++a)
     for (int k = 0; k < fks::kMaxN; ++k) tp->cfl1 &= tp->delta[a][k] >= -1 && tp->delta[a][k] <= 1;
+  if (with_shift && c->grid.dx > 0) {
+    const int a = c->grid.dx - 1;  // HALO faces exist only on the slowest axis
+    if (c->grid.bc[2 * a] == FKS_BC_HALO || c->grid.bc[2 * a + 1] == FKS_BC_HALO)
+      for (int k = 0; k < c->N; ++k)
+        if (tp->delta[a][k] < -1 || tp->delta[a][k] > 1) return FKS_E_UNSUPPORTED;
+  }
+  return FKS_OK;
 }
 
 fks::StepParams base_params(fks_ctx* c, const double* f_in, double* f_out, int mode) {
@@ -547,7 +557,7 @@ fks_status fks_set_stream(fks_ctx* c, void* s) {
 fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
   if (!c || !f || !Q || f == Q) return FKS_E_INVAL;
   fks::StepParams p = base_params(c, f, Q, 0);
-  fill_transport(c, &p.tp, false);
+  fill_transport(c, &p.tp, false);  // no shifts: cannot fail
   p.cell_list = nullptr;
   p.ncells = (int)c->ncells;
   return run_collision(c, p);
@@ -572,7 +582,8 @@ fks_status fks_transport(fks_ctx* c, const double* f_in, double* f_out, double d
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
   fks::TransportParams tp;
-  fill_transport(c, &tp, true);
+  st = fill_transport(c, &tp, true);
+  if (st != FKS_OK) return st;
   cudaError_t e = fks::launch_transport(f_in, f_out, tp, c->d_solid, c->ncells, c->n, c->N, c->dv, c->stream);
   c->launches++;
   if (e != cudaSuccess) return FKS_E_CUDA;
@@ -584,13 +595,14 @@ fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
+  fks::StepParams p = base_params(c, f_in, f_out, 1);
+  st = fill_transport(c, &p.tp, true);
+  if (st != FKS_OK) return st;
   if (c->nsolid) {
     if (fks::launch_copy_cells(f_in, f_out, c->d_solid_list, c->nsolid, c->n, c->stream) != cudaSuccess)
       return FKS_E_CUDA;
     c->launches++;
   }
-  fks::StepParams p = base_params(c, f_in, f_out, 1);
-  fill_transport(c, &p.tp, true);
   p.cell_list = c->nsolid ? c->d_fluid : nullptr;  // identity list: let the kernels prefetch
   p.ncells = c->nfluid;
   st = run_collision(c, p);
@@ -604,13 +616,15 @@ fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt
   if (nu_rule < FKS_NU_RHO || nu_rule > FKS_NU_EULER || (nu_rule == FKS_NU_CONST && !(mu > 0))) return FKS_E_INVAL;
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
+  fks::BgkParams p;
+  std::memset(&p, 0, sizeof(p));
+  st = fill_transport(c, &p.tp, true);
+  if (st != FKS_OK) return st;
   if (c->nsolid) {
     if (fks::launch_copy_cells(f_in, f_out, c->d_solid_list, c->nsolid, c->n, c->stream) != cudaSuccess)
       return FKS_E_CUDA;
     c->launches++;
   }
-  fks::BgkParams p;
-  std::memset(&p, 0, sizeof(p));
   p.f_in = f_in;
   p.f_out = f_out;
   p.nonfinite = c->d_flag;
@@ -622,7 +636,6 @@ fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt
   p.L = c->L;
   p.dv = 2.0 * c->L / c->N;
   std::memcpy(p.Ginv, c->Ginv, sizeof(p.Ginv));
-  fill_transport(c, &p.tp, true);
   cudaError_t e = fks::launch_bgk(c->N, c->dv, p, c->sm_count, c->stream);
   c->launches++;
   if (e != cudaSuccess) return FKS_E_CUDA;
@@ -669,7 +682,7 @@ static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, doubl
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, c->ev_in[i], 0);
     if (e != cudaSuccess) break;
     fks::StepParams p = base_params(c, c->d_host_in + off * n, c->d_host_out + off * n, 1);
-    fill_transport(c, &p.tp, true);
+    fill_transport(c, &p.tp, true);  // dx = 0: no shifts, cannot fail
     p.cell_list = nullptr;
     p.ncells = (int)cnt;
     st = run_collision(c, p);
@@ -690,9 +703,15 @@ static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, doubl
 fks_status fks_step_host(fks_ctx* c, const double* f_in_host, double* f_out_host, double dt) {
   if (!c || !f_in_host || !f_out_host) return FKS_E_INVAL;
   const size_t bytes = (size_t)c->ncells * c->n * sizeof(double);
-  if (!c->d_host_in) {
-    if (cudaMalloc(&c->d_host_in, bytes) != cudaSuccess) return FKS_E_NOMEM;
-    if (cudaMalloc(&c->d_host_out, bytes) != cudaSuccess) return FKS_E_NOMEM;
+  if (!c->d_host_in) {  // both buffers or neither: a half-allocated pair is never stored
+    double *in = nullptr, *out = nullptr;
+    if (cudaMalloc(&in, bytes) != cudaSuccess) return FKS_E_NOMEM;
+    if (cudaMalloc(&out, bytes) != cudaSuccess) {
+      cudaFree(in);
+      return FKS_E_NOMEM;
+    }
+    c->d_host_in = in;
+    c->d_host_out = out;
   }
   if (c->grid.dx == 0 && c->nsolid == 0) return step_host_pipelined(c, f_in_host, f_out_host, dt);
   if (cudaMemcpyAsync(c->d_host_in, f_in_host, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)

@@ -148,6 +148,12 @@ class DistributedStep:
         self.ctx, self.x = ctx, HaloExchange(slab, n, device, group=group)
 
     def __call__(self, f_in, f_out, dt):
+        import torch
+        # the exchange runs on torch's current stream: put the step on the same stream so the
+        # kernel reads the halo planes after the receive landed and the next exchange cannot
+        # overwrite them while the kernel still runs
+        if f_in.is_cuda:
+            self.ctx.set_stream(torch.cuda.current_stream(f_in.device))
         lo, hi = self.x.exchange(f_in)
         self.ctx.set_halo(lo, hi)
         self.ctx.step(f_in, f_out, dt)

@@ -304,13 +304,49 @@ def test_P11_projection_properties(d, N, L):
 
 # ---------------------------------------------------------------- P12: transport
 def test_shift_formula_examples(golden_dir):
-    """S:409-411 worked examples of s = floor(1/2 - d/dx)."""
+    """S:409-411 worked examples of s = floor(1/2 - d/dx), evaluated through the oracle's own
+    shift_s: N = 2 nodes v = -+L/2, dt = dx = 1 and n = 1, so d/dx = n (v dt)/dx = v_k with
+    L = 2|d/dx| (n = 0 for d = 0)."""
     for line in open(os.path.join(golden_dir, "shift_examples.txt")):
         line = line.split("#")[0].strip()
         if not line:
             continue
         r, s = line.split()
-        assert int(np.floor(0.5 - float(r))) == int(s)
+        r, s = float(r), int(s)
+        if r == 0.0:
+            got = transport.shift_s(0, 2, 1.0, 1.0, 1.0)
+            assert list(got) == [s, s]
+            continue
+        L = 2.0 * abs(r)
+        k = 1 if r > 0 else 0
+        assert abs(grid.nodes_1d(2, L)[k] - r) <= 4e-16 * abs(r)   # the node is d/dx (to rounding)
+        assert int(transport.shift_s(1, 2, L, 1.0, 1.0)[k]) == s
+
+
+def test_corner_ghost_precedence():
+    """Reading #19 at a domain corner: when the source leaves the domain through several axes the
+    lowest axis with a GHOST face supplies the value; an OUTFLOW axis only clamps."""
+    N, L, dx = 4, 2.0, 1.0
+    dt = 0.9 * dx / (L - L / N)                    # CFL 0.9: delta in {-1, 0, 1}
+    delta = transport.shift_delta(0, N, L, dt, dx)
+    kp = int(np.argmax(delta == -1))               # a velocity node with v > 0 (source one cell down)
+    assert delta[kp] == -1
+    F = RNG.random((3, 3, N, N))                   # [y, x, ky, kx]
+    g = {0: np.full((N, N), 10.0), 2: np.full((N, N), 20.0)}
+    G, O = transport.GHOST, transport.OUTFLOW
+    # cell (x, y) = (0, 0), velocity (kx, ky) = (kp, kp): source (-1, -1)
+    out = transport.gather(F, 0, 2, 2, N, L, dt, dx, [G, O, G, O], g)
+    assert out[0, 0, kp, kp] == 10.0               # both axes ghost: axis 0 wins
+    out = transport.gather(F, 0, 2, 2, N, L, dt, dx, [O, O, G, O], {2: g[2]})
+    assert out[0, 0, kp, kp] == 20.0               # axis 0 outflow (clamped), axis 1 ghost
+    out = transport.gather(F, 0, 2, 2, N, L, dt, dx, [G, O, O, O], {0: g[0]})
+    assert out[0, 0, kp, kp] == 10.0               # axis 0 ghost, axis 1 outflow
+    out = transport.gather(F, 0, 2, 2, N, L, dt, dx, [O, O, O, O], {})
+    assert out[0, 0, kp, kp] == F[0, 0, kp, kp]    # both clamped: the corner cell itself
+    # only the x shift leaves the domain (ky with delta 0): the ghost value regardless of y
+    k0 = int(np.argmax(delta == 0))
+    out = transport.gather(F, 0, 2, 2, N, L, dt, dx, [G, O, G, O], g)
+    assert out[1, 0, k0, kp] == 10.0
 
 
 def test_P12_free_transport_is_exact_periodic():

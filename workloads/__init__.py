@@ -6,4 +6,4 @@ velocity nodes and draws seeded random numbers.  Both the CUDA path and the orac
 its bytes; neither imports the other.
 """
 from .gen import (CONFIGS, config, initial_state, family, ghost_vectors, solid_mask,  # noqa: F401
-                  reentry_inflow_velocity, reentry_inflow_ghost)
+                  reentry_inflow_velocity, reentry_inflow_ghost, ScaledField)

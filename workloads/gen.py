@@ -106,7 +106,8 @@ def initial_state(c, ncells=None, start=0):
     if name in ("C4", "C5"):
         u = (3.0, 0.0, 0.0) if name == "C4" else (2.0, 0.0, 0.0)
         m = maxwellian(vs, 1.0, u, 1.0)
-        return np.broadcast_to(m, tuple(M) + m.shape).copy()
+        lead = tuple(M) if ncells is None else (ncells,)   # ncells: that many (flat) cells only
+        return np.broadcast_to(m, lead + m.shape).copy()
     raise KeyError(name)
 
 
@@ -192,3 +193,23 @@ def family(kind, dv, N, L, ncells, seed=0):
         else:
             raise ValueError(kind)
     return out
+
+
+class ScaledField:
+    """Lazy stand-in for a [cells..., (N,)*dv] array F[j] = s[j] * v (one fp64 product per element,
+    exactly what a device-side broadcast multiply computes), for full-size parity tests whose state
+    does not fit the host's numpy comfortably.  Supports .shape and the tuple indexing the oracle's
+    gathers use (spatial indices first, then velocity indices; integers or broadcastable arrays)."""
+
+    def __init__(self, v, s):
+        self.v = np.asarray(v, dtype=np.float64)
+        self.s = np.asarray(s, dtype=np.float64)
+        self.shape = self.s.shape + self.v.shape
+
+    def __getitem__(self, idx):
+        if not isinstance(idx, tuple):
+            idx = (idx,)
+        ns = self.s.ndim
+        sp, vel = idx[:ns], idx[ns:]
+        vel = vel + (slice(None),) * (self.v.ndim - len(vel))
+        return self.s[sp] * self.v[vel]
