@@ -78,3 +78,63 @@ def gaussian_mixture(centers, temps, masses):
             out += m * (2.0 * np.pi * T) ** (-d / 2.0) * np.exp(-r2 / (2.0 * T))
         return out
     return fun
+
+
+def carleman_Q(fun, v, d, gamma, C, R, nr=40, Kt=16, Kp=32, Ky=32, split=False):
+    """NEXT-3: Q(f)(v) straight from the paper's Carleman form (eq. defQBCarleman)
+    Q(v) = int int Btilde(x, y) delta(x . y) [f(v + y) f(v + x) - f(v + x + y) f(v)] dx dy
+    with the decoupled model Btilde(x, y) = 2^{d-1} C |x|^{gamma-(d-2)} (b = 1; reading #25)
+    and the spectral method's truncation |x|, |y| <= R (user units: R = R_scaled L / pi).
+
+    No Fourier anything: x = rho e (rho in [0, R] by Gauss-Jacobi with the rho^gamma weight that
+    remains after the Jacobian rho^{d-1} and delta(x . y) = delta(e . y) / rho; e over the whole
+    sphere: Gauss-Legendre in cos(theta) x uniform phi in 3D, uniform on S^1 in 2D), y over the
+    disk (3D, polar: r Gauss-Legendre x uniform angle) or the segment (2D) of radius R in e^perp."""
+    from .kernels import gauss_jacobi01
+    v = np.asarray(v, dtype=np.float64)
+    K = 2.0 ** (d - 1) * C
+    t, wt = gauss_jacobi01(nr, gamma)
+    rho, wrho = R * t, wt * R ** (gamma + 1.0)          # int_0^R rho^gamma g = sum wrho g(rho)
+    fv = fun(v[None, :])[0]
+    if d == 3:
+        es, we = _omega_3d(Kt, Kp)
+        xr, wr = np.polynomial.legendre.leggauss(nr)     # r in [0, R], weight r dr
+        r = 0.5 * R * (xr + 1.0)
+        wr = 0.5 * R * wr * r
+        ph = 2.0 * np.pi * np.arange(Ky) / Ky
+        gain = loss = 0.0
+        for e, w_e in zip(es, we):
+            a = np.array([1.0, 0.0, 0.0]) if abs(e[0]) < 0.9 else np.array([0.0, 1.0, 0.0])
+            e1 = np.cross(e, a)
+            e1 /= np.linalg.norm(e1)
+            e2 = np.cross(e, e1)
+            ys = (r[:, None, None] * (np.cos(ph)[None, :, None] * e1 + np.sin(ph)[None, :, None] * e2)).reshape(-1, 3)
+            wy = np.repeat(wr, Ky) * (2.0 * np.pi / Ky)
+            xs = rho[:, None] * e[None, :]                             # [nr, 3]
+            fy = fun(v[None, :] + ys)                                   # [ny]
+            fx = fun(v[None, :] + xs)                                   # [nr]
+            fxy = fun(v[None, None, :] + xs[:, None, :] + ys[None, :, :])  # [nr, ny]
+            gain += w_e * np.sum(wrho * fx * (fy @ wy))
+            loss += w_e * fv * np.sum(wrho * (fxy @ wy))
+    elif d == 2:
+        th = 2.0 * np.pi * np.arange(Kt * Kp) / (Kt * Kp)
+        xl, wl = np.polynomial.legendre.leggauss(2 * nr)            # y = s e_perp, s in [-R, R]
+        sy, wy = R * xl, R * wl
+        gain = loss = 0.0
+        for a in th:
+            e = np.array([np.cos(a), np.sin(a)])
+            ep = np.array([-np.sin(a), np.cos(a)])
+            ys = sy[:, None] * ep[None, :]
+            xs = rho[:, None] * e[None, :]
+            fy = fun(v[None, :] + ys)
+            fx = fun(v[None, :] + xs)
+            fxy = fun(v[None, None, :] + xs[:, None, :] + ys[None, :, :])
+            w_e = 2.0 * np.pi / (Kt * Kp)
+            gain += w_e * np.sum(wrho * fx * (fy @ wy))
+            loss += w_e * fv * np.sum(wrho * (fxy @ wy))
+    else:
+        raise ValueError(d)
+    gain, loss = K * gain, K * loss
+    if split:
+        return gain, loss
+    return gain - loss

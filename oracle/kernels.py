@@ -65,6 +65,65 @@ def psi3_printed(s, R):
     return 2.0 * R * R * sinc(0.5 * R * s) ** 2
 
 
+# ---------------------------------------------------------------- NEXT-3: general decoupled kernels
+def gauss_jacobi01(n, gamma):
+    """Nodes t_i, weights w_i with sum_i w_i g(t_i) = int_0^1 t^gamma g(t) dt exactly for polynomials
+    g of degree <= 2n-1 (gamma > -1).  Golub-Welsch: the nodes are the eigenvalues of the Jacobi
+    matrix of the Jacobi polynomials P^(0, gamma) on [-1, 1] (numpy eigvalsh as the library
+    primitive), polished by Newton on the orthonormal three-term recurrence; the weights come from
+    the Christoffel sum w_i = 1 / sum_{k<n} q_k(x_i)^2 (accurate to a few ulp); t = (1 + x) / 2."""
+    a, b = 0.0, float(gamma)
+    k = np.arange(n, dtype=np.float64)
+    ab = a + b
+    alpha = np.empty(n)
+    alpha[0] = (b - a) / (ab + 2.0)
+    kk = k[1:]
+    alpha[1:] = (b * b - a * a) / ((2 * kk + ab) * (2 * kk + ab + 2.0))
+    kk = np.arange(1, n + 1, dtype=np.float64)   # beta_1 .. beta_n
+    beta = 4.0 * kk * (kk + a) * (kk + b) * (kk + ab) / ((2 * kk + ab) ** 2 * (2 * kk + ab + 1.0) * (2 * kk + ab - 1.0))
+    sb = np.sqrt(beta)
+    from scipy.special import gammaln
+    mu0 = np.exp((ab + 1.0) * np.log(2.0) + gammaln(a + 1.0) + gammaln(b + 1.0) - gammaln(ab + 2.0))
+    J = np.diag(alpha) + np.diag(sb[:-1], 1) + np.diag(sb[:-1], -1)
+    x = np.sort(np.linalg.eigvalsh(J))
+
+    def recur(x):
+        """q_0..q_n and q_n' at the points x (orthonormal recurrence)."""
+        qm, q = np.zeros_like(x), np.full_like(x, 1.0 / np.sqrt(mu0))
+        dm, dq = np.zeros_like(x), np.zeros_like(x)
+        ssum = q * q
+        for j in range(n):
+            qn = ((x - alpha[j]) * q - (sb[j - 1] if j else 0.0) * qm) / sb[j]
+            dn = (q + (x - alpha[j]) * dq - (sb[j - 1] if j else 0.0) * dm) / sb[j]
+            qm, q, dm, dq = q, qn, dq, dn
+            if j < n - 1:
+                ssum = ssum + q * q
+        return q, dq, ssum
+
+    for _ in range(3):
+        qn, dqn, _ = recur(x)
+        x = x - qn / dqn
+    _, _, ssum = recur(x)
+    w = 1.0 / ssum
+    return 0.5 * (1.0 + x), w * 2.0 ** (-b - 1.0)
+
+
+def phi_a(s, R, gamma, nodes=160):
+    """NEXT-3 (P:498-509, P:537-538 with reading #4): phi_{R,a}(s) = int_{-R}^{R} |rho|^gamma e^{i rho s}
+    d rho = 2 R^{gamma+1} int_0^1 t^gamma cos(R s t) dt, the radial factor of the decoupled kernel
+    Btilde(x, y) = 2^{d-1} C |x|^{gamma-(d-2)} b(|y|), b = 1 (d = 3: |rho| a(|rho|) with
+    a = |rho|^{gamma-1}; d = 2: a(|rho|) = |rho|^gamma).  gamma = 1 (d = 3) gives phi3, gamma = 0
+    gives phi2.  Evaluated by Gauss-Jacobi quadrature with the t^gamma weight (gamma > -1)."""
+    s = np.asarray(s, dtype=np.float64)
+    t, w = gauss_jacobi01(nodes, gamma)
+    z = (R * s).reshape(-1)
+    out = np.empty(z.shape)
+    for c0 in range(0, z.size, 65536):
+        zz = z[c0:c0 + 65536]
+        out[c0:c0 + 65536] = np.cos(np.multiply.outer(zz, t)) @ w
+    return (2.0 * R ** (gamma + 1.0) * out).reshape(s.shape)
+
+
 def directions_2d(A):
     """(e [A,2], e_perp [A,2], w [A]) with theta_p = pi p / A, p = 1..A, w = pi/A."""
     th = np.pi * np.arange(1, A + 1) / A

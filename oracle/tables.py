@@ -50,25 +50,31 @@ def default_R():
 
 
 def build_tables(d, N, L, directions=None, A=8, R=None, kernel_const=None, psi="derived",
-                 symmetrise=True):
+                 symmetrise=True, gamma=None):
     """Build the tables for d=2 (Maxwell molecules, gamma=0) or d=3 (hard spheres, gamma=1).
 
     directions: for d=2 the number A of angles is used; for d=3 a tuple (e, w) of
     unit vectors [A,3] and weights [A] (default: the 24-point design, reading #17).
+    gamma (NEXT-3, reading #25): VHS exponent of B = C |q|^gamma; at gamma = d - 2 the
+    Carleman kernel is constant and the tables are the closed forms above; any other
+    gamma > -1 uses the decoupled model Btilde(x, y) = 2^{d-1} C |x|^{gamma-(d-2)} (b = 1), i.e.
+    alpha_p = phi_{R,a}(l . e_p) by quadrature (kernels.phi_a) and alpha'_p
+    unchanged (phi2 in 2D, psi3 in 3D).
     """
     if R is None:
         R = default_R()
     kappa = np.pi / L
     ls = grid.mode_vectors(d, N)
     if d == 2:
-        gamma = 0.0
+        gamma = 0.0 if gamma is None else float(gamma)
         b0 = 1.0 / (2.0 * np.pi) if kernel_const is None else kernel_const
         Btilde = 2.0 * b0
         e, ep, w = kernels.directions_2d(A)
-        alpha = np.stack([kernels.phi2(ls[0] * e[p, 0] + ls[1] * e[p, 1], R) for p in range(len(w))])
+        rad = (lambda s: kernels.phi2(s, R)) if gamma == 0.0 else (lambda s: kernels.phi_a(s, R, gamma))
+        alpha = np.stack([rad(ls[0] * e[p, 0] + ls[1] * e[p, 1]) for p in range(len(w))])
         alphap = np.stack([kernels.phi2(ls[0] * ep[p, 0] + ls[1] * ep[p, 1], R) for p in range(len(w))])
     elif d == 3:
-        gamma = 1.0
+        gamma = 1.0 if gamma is None else float(gamma)
         C1 = 1.0 / (4.0 * np.pi) if kernel_const is None else kernel_const
         Btilde = 4.0 * C1
         if directions is None:
@@ -84,7 +90,7 @@ def build_tables(d, N, L, directions=None, A=8, R=None, kernel_const=None, psi="
             cy = ls[2] * ex - ls[0] * ez
             cz = ls[0] * ey - ls[1] * ex
             perp = np.sqrt(cx * cx + cy * cy + cz * cz)
-            al.append(kernels.phi3(dot, R))
+            al.append(kernels.phi3(dot, R) if gamma == 1.0 else kernels.phi_a(dot, R, gamma))
             alp.append(psif(perp, R))
         alpha, alphap = np.stack(al), np.stack(alp)
     else:
