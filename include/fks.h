@@ -74,8 +74,13 @@ typedef struct {
  *                 (P:490); dv = 3 -> 24 = the spherical 7-design (reading #17), a perfect
  *                 square A1^2 = the (theta, phi) product grid of P:527-540 (reading #6);
  *                 anything else needs fks_set_dirs.
- *   kernel_gamma  VHS exponent alpha: must be 0 for dv = 2 and 1 for dv = 3, the
- *                 two cases where Btilde is constant; otherwise FKS_E_UNSUPPORTED.
+ *   kernel_gamma  VHS exponent gamma of B = C |q|^gamma (the paper's alpha), -1 < gamma <= 2,
+ *                 else FKS_E_UNSUPPORTED.  gamma = dv - 2 (2D Maxwell molecules, 3D hard spheres)
+ *                 makes Btilde constant and the tables closed forms;
+ *                 any other gamma uses the decoupled model Btilde(x, y) = 2^{dv-1} C |x|^{gamma-(dv-2)},
+ *                 b = 1 (NEXT-3, reading #25): alpha_p = phi_{R,a}(l . e_p) with
+ *                 phi_{R,a}(s) = int_{-R}^{R} |rho|^gamma e^{i rho s} d rho by 160-point Gauss-Jacobi
+ *                 quadrature, alpha'_p unchanged; the kernels are the same.
  * Defaults: tau = 1, b0 = 1/(2 pi) (2D) or C1 = 1/(4 pi) (3D) (reading #7), R = 2 lambda pi
  * (reading #1), projection on.  Builds the fp64 tables on the host and uploads them.
  * Returns FKS_E_CUDA if no sm_100 device is present. */
@@ -164,8 +169,8 @@ const char* fks_strerror(fks_status s);
  * w_host: [A], e_host: [A][dv].  Arrays may be NULL.  Returns the node-space factor
  * s = Btilde kappa^{-(dv+gamma)} in *scale.  Arguments as in fks_init / fks_set_params. */
 fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, double kernel_const,
-                           double* alpha_host, double* alphap_host, double* D_host, double* w_host,
-                           double* e_host, double* scale);
+                           double kernel_gamma, double* alpha_host, double* alphap_host, double* D_host,
+                           double* w_host, double* e_host, double* scale);
 
 /* delta_k = s^{n+1}_k - s^n_k for the N nodes of one velocity axis (a1). */
 fks_status fks_host_shift(int64_t n, int Nv, double L, double dt, double h, int8_t* delta_host);

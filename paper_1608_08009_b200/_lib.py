@@ -38,8 +38,8 @@ SIGNATURES = {
     "fks_launch_count": (c_int64, [c_void_p]),
     "fks_finalize": (c_int, [c_void_p]),
     "fks_strerror": (ctypes.c_char_p, [c_int]),
-    "fks_host_tables": (c_int, [c_int, c_int, c_double, c_int, c_double, c_double, P_DOUBLE, P_DOUBLE, P_DOUBLE,
-                                P_DOUBLE, P_DOUBLE, P_DOUBLE]),
+    "fks_host_tables": (c_int, [c_int, c_int, c_double, c_int, c_double, c_double, c_double, P_DOUBLE, P_DOUBLE,
+                                P_DOUBLE, P_DOUBLE, P_DOUBLE, P_DOUBLE]),
     "fks_host_shift": (c_int, [c_int64, c_int, c_double, c_double, c_double, ctypes.POINTER(ctypes.c_int8)]),
 }
 

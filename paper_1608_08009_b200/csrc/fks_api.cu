@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/fks.h"
@@ -38,6 +39,77 @@ double phi3(double s, double R) {
 }
 // Reading #2 (P:501-506 derivation): psi(s) = 2 pi R J1(R s) / s, psi(0) = pi R^2
 double psi3(double s, double R) { return s == 0.0 ? kPi * R * R : 2.0 * kPi * R * ::j1(R * s) / s; }
+
+// NEXT-3 (reading #25): phi_{R,a}(s) = int_{-R}^{R} |rho|^gamma e^{i rho s} d rho
+// = 2 R^{gamma+1} int_0^1 t^gamma cos(R s t) dt, by an n-point Gauss-Jacobi
+// rule for the weight t^gamma.  Nodes: eigenvalues of the Jacobi matrix of P^(0,gamma) found by
+// Sturm-sequence bisection, polished by Newton on the orthonormal recurrence; weights from the
+// Christoffel sum 1 / sum_k q_k(x)^2.
+struct GaussJacobi {
+  std::vector<double> t, w;  // nodes in (0, 1), weights for int_0^1 t^gamma g(t) dt
+};
+
+GaussJacobi gauss_jacobi01(int n, double gamma) {
+  const double a = 0.0, b = gamma, ab = a + b;
+  std::vector<double> al(n), sb(n);  // diagonal alpha_k, off-diagonal sqrt(beta_{k+1})
+  for (int k = 0; k < n; ++k) {
+    al[k] = k == 0 ? (b - a) / (ab + 2.0) : (b * b - a * a) / ((2.0 * k + ab) * (2.0 * k + ab + 2.0));
+    const double j = k + 1.0;
+    sb[k] = std::sqrt(4.0 * j * (j + a) * (j + b) * (j + ab) /
+                      ((2.0 * j + ab) * (2.0 * j + ab) * (2.0 * j + ab + 1.0) * (2.0 * j + ab - 1.0)));
+  }
+  const double mu0 = std::exp((ab + 1.0) * std::log(2.0) + std::lgamma(a + 1.0) + std::lgamma(b + 1.0) -
+                              std::lgamma(ab + 2.0));
+  auto below = [&](double x) {  // number of eigenvalues < x (Sturm sequence of J - x)
+    int cnt = 0;
+    double d = 1.0;
+    for (int k = 0; k < n; ++k) {
+      d = (al[k] - x) - (k ? sb[k - 1] * sb[k - 1] / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      if (d < 0.0) ++cnt;
+    }
+    return cnt;
+  };
+  // q_n(x), q_n'(x) and sum_{k<n} q_k(x)^2 by the orthonormal three-term recurrence
+  auto recur = [&](double x, double* qn, double* dqn, double* ssum) {
+    double qm = 0.0, q = 1.0 / std::sqrt(mu0), dm = 0.0, dq = 0.0, s = q * q;
+    for (int k = 0; k < n; ++k) {
+      const double prev = k ? sb[k - 1] : 0.0;
+      const double q1 = ((x - al[k]) * q - prev * qm) / sb[k];
+      const double d1 = (q + (x - al[k]) * dq - prev * dm) / sb[k];
+      qm = q; q = q1; dm = dq; dq = d1;
+      if (k < n - 1) s += q * q;
+    }
+    *qn = q; *dqn = dq; *ssum = s;
+  };
+  GaussJacobi g;
+  g.t.resize(n);
+  g.w.resize(n);
+  for (int i = 0; i < n; ++i) {
+    double lo = -1.0, hi = 1.0;
+    for (int it = 0; it < 200 && hi - lo > 1e-17; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (below(mid) > i) hi = mid; else lo = mid;
+    }
+    double x = 0.5 * (lo + hi), qn, dqn, ss;
+    for (int it = 0; it < 3; ++it) {
+      recur(x, &qn, &dqn, &ss);
+      x -= qn / dqn;
+    }
+    recur(x, &qn, &dqn, &ss);
+    g.t[i] = 0.5 * (1.0 + x);
+    g.w[i] = std::exp2(-b - 1.0) / ss;
+  }
+  return g;
+}
+
+constexpr int kJacobiNodes = 160;  // exact for cos(z t) to rounding up to z ~ 300 (N = 64: z <= 160)
+
+double phi_a(double s, double R, double gamma, const GaussJacobi& g) {
+  double acc = 0.0;
+  for (size_t i = 0; i < g.t.size(); ++i) acc += g.w[i] * std::cos(R * s * g.t[i]);
+  return 2.0 * std::pow(R, gamma + 1.0) * acc;
+}
 
 // ------------------------------------------------------------------ direction sets
 Dirs dirs_2d(int A) {  // P:490 theta_p = pi p / A, weight pi / A (reading #5)
@@ -115,26 +187,35 @@ bool default_dirs(int dv, int M, Dirs* out) {
 
 int mu(int j, int N) { return j < N / 2 ? j : j - N; }
 
+// The Carleman kernel is constant -- closed-form radial functions -- exactly when gamma = d - 2
+// (2D Maxwell molecules, 3D hard spheres); otherwise the decoupled model of reading #25.
+bool exact_gamma(int dv, double gamma) { return gamma == (double)(dv - 2); }
+
 // Unfolded tables: alpha, alphap [A][n] in FFT mode order, symmetrised over
-// l -> -l (reading #10), and D = sum_p w_p alpha_p alpha'_p.
-void build_tables(int dv, int N, double R, const Dirs& dirs, std::vector<double>& alpha, std::vector<double>& alphap,
-                  std::vector<double>& D) {
+// l -> -l (reading #10), and D = sum_p w_p alpha_p alpha'_p.  Directions are built in parallel
+// host threads (the general-gamma radial function is a 160-point quadrature per entry).
+void build_tables(int dv, int N, double R, double gamma, const Dirs& dirs, std::vector<double>& alpha,
+                  std::vector<double>& alphap, std::vector<double>& D) {
   const int A = (int)dirs.w.size();
   const int n = dv == 3 ? N * N * N : N * N;
   alpha.assign((size_t)A * n, 0.0);
   alphap.assign((size_t)A * n, 0.0);
-  std::vector<double> ra(n), rb(n);
-  for (int p = 0; p < A; ++p) {
+  const bool exact = exact_gamma(dv, gamma);
+  GaussJacobi gj;
+  if (!exact) gj = gauss_jacobi01(kJacobiNodes, gamma);
+  auto one_dir = [&](int p) {
+    std::vector<double> ra(n), rb(n);
     const double* e = &dirs.e[(size_t)p * dv];
     for (int k = 0; k < n; ++k) {
       const double lx = mu(k % N, N), ly = mu((k / N) % N, N), lz = dv == 3 ? mu(k / (N * N), N) : 0.0;
       if (dv == 2) {
-        ra[k] = phi2(lx * e[0] + ly * e[1], R);
+        const double dot = lx * e[0] + ly * e[1];
+        ra[k] = exact ? phi2(dot, R) : phi_a(dot, R, gamma, gj);
         rb[k] = phi2(-lx * e[1] + ly * e[0], R);  // e_perp = e_{theta + pi/2}
       } else {
         const double dot = lx * e[0] + ly * e[1] + lz * e[2];
         const double cx = ly * e[2] - lz * e[1], cy = lz * e[0] - lx * e[2], cz = lx * e[1] - ly * e[0];
-        ra[k] = phi3(dot, R);
+        ra[k] = exact ? phi3(dot, R) : phi_a(dot, R, gamma, gj);
         rb[k] = psi3(std::sqrt(cx * cx + cy * cy + cz * cz), R);
       }
     }
@@ -145,17 +226,28 @@ void build_tables(int dv, int N, double R, const Dirs& dirs, std::vector<double>
       alpha[(size_t)p * n + k] = 0.5 * (ra[k] + ra[km]);
       alphap[(size_t)p * n + k] = 0.5 * (rb[k] + rb[km]);
     }
-  }
+  };
+  const int nth = std::max(1, std::min<int>(A, (int)std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nth; ++t)
+    pool.emplace_back([&, t]() {
+      for (int p = t; p < A; p += nth) one_dir(p);
+    });
+  for (auto& th : pool) th.join();
   D.assign(n, 0.0);
   for (int p = 0; p < A; ++p)
     for (int k = 0; k < n; ++k) D[k] += dirs.w[p] * alpha[(size_t)p * n + k] * alphap[(size_t)p * n + k];
 }
 
-// s = Btilde kappa^-(d+gamma), Btilde = 2^{d-1} b (reading #3): 2D 2 b0 (L/pi)^2, 3D 4 C1 (L/pi)^4.
-double node_scale(int dv, double L, double kconst) {
+// s = Btilde kappa^-(d+gamma), Btilde = 2^{d-1} C (reading #3): 2D Maxwell 2 b0 (L/pi)^2, 3D hard
+// spheres 4 C1 (L/pi)^4; any gamma (reading #25): 2^{d-1} C (L/pi)^{d+gamma}.
+double node_scale(int dv, double L, double kconst, double gamma) {
   const double k = L / kPi;
-  return dv == 2 ? 2.0 * kconst * k * k : 4.0 * kconst * k * k * k * k;
+  if (exact_gamma(dv, gamma)) return dv == 2 ? 2.0 * kconst * k * k : 4.0 * kconst * k * k * k * k;
+  return (dv == 2 ? 2.0 : 4.0) * kconst * std::pow(k, dv + gamma);
 }
+
+bool valid_gamma(double g) { return g > -1.0 && g <= 2.0; }
 
 double default_kconst(int dv) { return dv == 2 ? 1.0 / (2.0 * kPi) : 1.0 / (4.0 * kPi); }
 
@@ -240,9 +332,9 @@ fks_status cuda_fail(cudaError_t e) { return e == cudaSuccess ? FKS_OK : FKS_E_C
 
 fks_status upload_tables(fks_ctx* c) {
   std::vector<double> al, alp, D;
-  build_tables(c->dv, c->N, c->R, c->dirs, al, alp, D);
+  build_tables(c->dv, c->N, c->R, c->gamma, c->dirs, al, alp, D);
   const int n = c->n, N = c->N, A = c->A;
-  const double s = node_scale(c->dv, c->L, c->kconst);
+  const double s = node_scale(c->dv, c->L, c->kconst, c->gamma);
   // Fold s, w_p and 1/n (the kernels use the unnormalised forward DFT) into the tables.
   auto folded = [&](int p, int k) {
     return p < A ? make_double2(s * c->dirs.w[p] * al[(size_t)p * n + k] / n, alp[(size_t)p * n + k] / n)
@@ -405,21 +497,23 @@ const char* fks_strerror(fks_status s) {
   return "unknown status";
 }
 
-fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, double kernel_const, double* alpha_host,
-                           double* alphap_host, double* D_host, double* w_host, double* e_host, double* scale) {
+fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, double kernel_const, double kernel_gamma,
+                           double* alpha_host, double* alphap_host, double* D_host, double* w_host, double* e_host,
+                           double* scale) {
   if ((dv != 2 && dv != 3) || !valid_N(Nv) || !(L > 0)) return FKS_E_INVAL;
+  if (!valid_gamma(kernel_gamma)) return FKS_E_UNSUPPORTED;
   Dirs d;
   if (!default_dirs(dv, M_dirs, &d)) return FKS_E_UNSUPPORTED;
   if (!(R > 0)) R = 2.0 * kLambda * kPi;
   if (!(kernel_const > 0)) kernel_const = default_kconst(dv);
   std::vector<double> al, alp, D;
-  build_tables(dv, Nv, R, d, al, alp, D);
+  build_tables(dv, Nv, R, kernel_gamma, d, al, alp, D);
   if (alpha_host) std::memcpy(alpha_host, al.data(), al.size() * sizeof(double));
   if (alphap_host) std::memcpy(alphap_host, alp.data(), alp.size() * sizeof(double));
   if (D_host) std::memcpy(D_host, D.data(), D.size() * sizeof(double));
   if (w_host) std::memcpy(w_host, d.w.data(), d.w.size() * sizeof(double));
   if (e_host) std::memcpy(e_host, d.e.data(), d.e.size() * sizeof(double));
-  if (scale) *scale = node_scale(dv, L, kernel_const);
+  if (scale) *scale = node_scale(dv, L, kernel_const, kernel_gamma);
   return FKS_OK;
 }
 
@@ -435,7 +529,7 @@ fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double k
   const int dv = grid->dv;
   if ((dv != 2 && dv != 3) || !valid_N(Nv) || !(L > 0) || grid->dx < 0 || grid->dx > 3 || grid->dx > dv)
     return FKS_E_INVAL;
-  if ((dv == 2 && kernel_gamma != 0.0) || (dv == 3 && kernel_gamma != 1.0)) return FKS_E_UNSUPPORTED;
+  if (!valid_gamma(kernel_gamma)) return FKS_E_UNSUPPORTED;  // NEXT-3: -1 < gamma <= 2 (reading #25)
   int64_t ncells = 1;
   const int axes = grid->dx == 0 ? 1 : grid->dx;
   for (int a = 0; a < axes; ++a) {

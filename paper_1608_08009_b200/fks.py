@@ -156,15 +156,18 @@ def fks_finalize(ctx):
     ctx.close()
 
 
-def host_tables(dv, Nv, L, M_dirs, R=0.0, kernel_const=0.0):
+def host_tables(dv, Nv, L, M_dirs, R=0.0, kernel_const=0.0, kernel_gamma=None):
     """fks_host_tables: (alpha [A, n], alphap [A, n], D [n], w [A], e [A, dv], scale)."""
     lib = load()
+    if kernel_gamma is None:
+        kernel_gamma = 0.0 if dv == 2 else 1.0
     A = M_dirs
     n = Nv ** dv
     al, alp = np.zeros((A, n)), np.zeros((A, n))
     D, w, e = np.zeros(n), np.zeros(A), np.zeros((A, dv))
     s = ctypes.c_double()
-    check(lib.fks_host_tables(dv, Nv, float(L), M_dirs, float(R), float(kernel_const), _dptr(al), _dptr(alp),
+    check(lib.fks_host_tables(dv, Nv, float(L), M_dirs, float(R), float(kernel_const), float(kernel_gamma),
+                              _dptr(al), _dptr(alp),
                               _dptr(D), _dptr(w), _dptr(e), ctypes.byref(s)), "fks_host_tables")
     return al, alp, D, w, e, s.value
 

@@ -37,19 +37,22 @@ def test_strerror(fks):
         assert lib.fks_strerror(s)
 
 
-@pytest.mark.parametrize("dv,N,L,A", [(2, 8, 4.0, 8), (2, 16, 6.0, 8), (2, 32, 9.0, 8), (3, 8, 7.0, 24),
-                                      (3, 16, 7.0, 24), (3, 8, 7.0, 64)])
-def test_host_tables_match_oracle(fks, dv, N, L, A):
+@pytest.mark.parametrize("dv,N,L,A,gamma", [(2, 8, 4.0, 8, None), (2, 16, 6.0, 8, None), (2, 32, 9.0, 8, None),
+                                            (3, 8, 7.0, 24, None), (3, 16, 7.0, 24, None), (3, 8, 7.0, 64, None),
+                                            (3, 16, 7.0, 24, 0.0), (3, 8, 7.0, 24, 0.5), (3, 16, 7.0, 64, 2.0),
+                                            (3, 8, 7.0, 24, -0.5), (2, 32, 9.0, 8, 1.0), (2, 16, 6.0, 8, 0.3)])
+def test_host_tables_match_oracle(fks, dv, N, L, A, gamma):
     """Two independent table builders (C++ in the library, numpy in the oracle) agree to a few
     ulp: phi/psi (P:475, P:524, reading #2), directions (P:490, reading #17, reading #6),
-    symmetrisation (reading #10) and D."""
-    al, alp, D, w, e, s = fks.host_tables(dv, N, L, A)
+    symmetrisation (reading #10) and D; for general gamma (NEXT-3, reading #25) the quadrature
+    phi_{R,a} (Sturm bisection + Newton in the library, numpy eigvalsh + Newton in the oracle)."""
+    al, alp, D, w, e, s = fks.host_tables(dv, N, L, A, kernel_gamma=gamma)
     if dv == 2:
-        ref = otab.build_tables(2, N, L, A=A)
+        ref = otab.build_tables(2, N, L, A=A, gamma=gamma)
     elif A == 24:
-        ref = otab.build_tables(3, N, L)
+        ref = otab.build_tables(3, N, L, gamma=gamma)
     else:
-        ref = otab.build_tables(3, N, L, directions=okern.directions_3d_product(8, 8))
+        ref = otab.build_tables(3, N, L, directions=okern.directions_3d_product(8, 8), gamma=gamma)
     np.testing.assert_allclose(w, ref.w, rtol=1e-14, atol=0)
     for p in range(A):
         scale = np.abs(ref.alpha[p]).max()
@@ -98,7 +101,10 @@ def test_init_argument_validation(fks):
         fks.Context(3, 0, [4], 12, 7.0, 24)          # N not in {8,16,32}
     assert ei.value.status == -1
     with pytest.raises(fks.FksError) as ei:
-        fks.Context(3, 0, [4], 8, 7.0, 24, kernel_gamma=0.5)   # non-decoupled VHS
+        fks.Context(3, 0, [4], 8, 7.0, 24, kernel_gamma=2.5)   # outside -1 < gamma <= 2 (reading #25)
+    assert ei.value.status == -2
+    with pytest.raises(fks.FksError) as ei:
+        fks.Context(2, 0, [4], 8, 7.0, 8, kernel_gamma=-1.0)   # phi_{R,a} diverges at gamma = -1
     assert ei.value.status == -2
     with pytest.raises(fks.FksError) as ei:
         fks.Context(3, 0, [4], 8, 7.0, 23)           # no built-in 23-direction set
