@@ -37,15 +37,32 @@ def shift_delta(n, N, L, dt, dx):
     return shift_s(n + 1, N, L, dt, dx) - shift_s(n, N, L, dt, dx)
 
 
-def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None, cells=None):
+def shift_s_half(p, N, L, dt, dx):
+    """NEXT-4 (Strang splitting): the shift at the half-step position p (time p dt / 2),
+    s = floor(0.5 - (p * c) * 0.5), c = (v_k dt) / dx.  For even p = 2n this is bitwise shift_s(n)
+    (scaling by 2 and by 1/2 is exact in binary floating point)."""
+    v = grid.nodes_1d(N, L)
+    c = (v * dt) / dx
+    t = (np.float64(p) * c) * 0.5
+    return np.floor(0.5 - t).astype(np.int64)
+
+
+def shift_delta_half(p, N, L, dt, dx):
+    """delta_k from half-step position p to p + 1 (a transport over dt / 2)."""
+    return shift_s_half(p + 1, N, L, dt, dx) - shift_s_half(p, N, L, dt, dx)
+
+
+def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None, cells=None, delta=None):
     """f* from F^n.  bc: list of 2*dxdim face kinds [lo0, hi0, lo1, hi1, ...].
     ghosts: dict face -> ghost vector of shape (N,)*dv.  cells: optional flat cell indices; then
-    only those cells are computed and returned as [len(cells), (N,)*dv]."""
+    only those cells are computed and returned as [len(cells), (N,)*dv].  delta: the per-node
+    shift table to use instead of shift_delta(n) (Strang half steps)."""
     if dxdim == 0:
         return F.copy() if cells is None else F.reshape((-1,) + F.shape[dxdim:])[list(cells)].copy()
     sp_shape = F.shape[:dxdim]          # (M_{dx-1}, ..., M_0)
     M = sp_shape[::-1]                  # M[a] = cells along space axis a
-    delta = shift_delta(n, N, L, dt, dx)
+    if delta is None:
+        delta = shift_delta(n, N, L, dt, dx)
     vshape = (N,) * dv
     out = np.empty_like(F) if cells is None else None
     # velocity-axis index array per component a: component a is array axis dv-1-a
@@ -86,7 +103,7 @@ def gather(F, n, dxdim, dv, N, L, dt, dx, bc, ghosts=None, cells=None):
     return out if sub is None else sub
 
 
-def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid, cells=None):
+def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid, cells=None, delta=None):
     """NEXT-1: f* with specular reflection at solid cells ("reflective boundary conditions",
     S:430-438 apply_solid_reflection; reading #23 of DESIGN.md).
 
@@ -105,7 +122,8 @@ def gather_specular(F, n, dxd, dv, N, L, dt, dx, bc, ghosts, solid, cells=None):
     [len(cells), (N,)*dv] (F may then be any object with .shape and integer-tuple indexing)."""
     sp_shape = F.shape[:dxd]
     M = sp_shape[::-1]
-    delta = shift_delta(n, N, L, dt, dx)
+    if delta is None:
+        delta = shift_delta(n, N, L, dt, dx)
     out = np.empty_like(F) if cells is None else np.empty((len(cells),) + (N,) * dv)
 
     def in_domain_solid(cell):                               # cell: list of dxd coordinates
