@@ -115,6 +115,21 @@ fks_status fks_set_solid(fks_ctx* ctx, const uint8_t* solid_host);
  * default.  FKS_E_UNSUPPORTED with HALO faces (a partitioned grid). */
 fks_status fks_set_specular(fks_ctx* ctx, int on);
 
+/* NEXT-4 (reading #26): the time scheme of fks_step.
+ *   splitting  FKS_SPLIT_LIE (default; transport then collision) or FKS_SPLIT_STRANG
+ *              ("high order time splitting": f^{n+1} = T(dt/2) C(dt) T(dt/2) f^n, the
+ *              half transports being FKS gathers between the half-step positions 2n -> 2n+1 -> 2n+2,
+ *              s = floor(1/2 - (p c) / 2); identical to Lie without spatial axes).
+ *   integrator FKS_TIME_EULER (default; eq. f_coll) or FKS_TIME_HEUN ("many
+ *              different time integrators can be employed": explicit RK2, f1 = f* + dt/tau PiQ(f*),
+ *              f^{n+1} = (f* + f1 + dt/tau PiQ(f1)) / 2 -- two collision passes per step).
+ * Non-default schemes use one library-owned state-sized scratch buffer (allocated on first use).
+ * FKS_E_UNSUPPORTED for Strang on a partitioned grid (HALO faces: the second half transport would
+ * need a second exchange); fks_step_bgk supports Strang but not Heun (FKS_E_UNSUPPORTED). */
+enum { FKS_SPLIT_LIE = 0, FKS_SPLIT_STRANG = 1 };
+enum { FKS_TIME_EULER = 0, FKS_TIME_HEUN = 1 };
+fks_status fks_set_scheme(fks_ctx* ctx, int splitting, int integrator);
+
 /* Stream (a cudaStream_t passed as void*) on which all later work is enqueued. */
 fks_status fks_set_stream(fks_ctx* ctx, void* cuda_stream);
 
@@ -126,7 +141,8 @@ fks_status fks_collide(fks_ctx* ctx, const double* f, double* Q);
  * dt must equal the context dt once one was set (it is fixed per run, reading #15). */
 fks_status fks_transport(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
 
-/* a1..a9 fused: f_out = F^{n+1} from f_in = F^n, then n += 1.  f_out != f_in. */
+/* a1..a9 fused: f_out = F^{n+1} from f_in = F^n, then n += 1.  f_out != f_in.  One launch (plus a
+ * solid-cell copy when the grid has solids) with the default scheme; see fks_set_scheme. */
 fks_status fks_step(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
 
 /* fks_step with HOST buffers: copies f_in_host to the device, steps, copies the result back

@@ -23,8 +23,12 @@ def _transport(F, n, cfg, delta=None):
     if cfg.get("specular"):
         return transport.gather_specular(F, n, dxd, dv, N, L, cfg["dt"], cfg.get("dx", 1.0), cfg.get("bc"),
                                          cfg.get("ghosts") or {}, cfg["solid"], delta=delta)
-    return transport.gather(F, n, dxd, dv, N, L, cfg["dt"], cfg.get("dx", 1.0), cfg.get("bc"), cfg.get("ghosts"),
-                            delta=delta)
+    out = transport.gather(F, n, dxd, dv, N, L, cfg["dt"], cfg.get("dx", 1.0), cfg.get("bc"), cfg.get("ghosts"),
+                           delta=delta)
+    solid = cfg.get("solid")
+    if solid is not None:               # reading #19: solid cells keep their values
+        out[solid] = F[solid]
+    return out
 
 
 def _collision_update(fj, cfg, tab, coll, integrator):
@@ -51,7 +55,7 @@ def _collide_all(Fs, F, cfg, tab, evaluator, integrator):
     for jflat in range(int(np.prod(sp_shape)) if dxd else 1):
         jidx = np.unravel_index(jflat, sp_shape) if dxd else ()
         if solid is not None and solid[jidx]:
-            out[jidx] = Fs[jidx]
+            out[jidx] = F[jidx]          # reading #19: solid cells keep their values
             continue
         out[jidx] = _collision_update(Fs[jidx], cfg, tab, coll, integrator)
     return out

@@ -31,6 +31,7 @@ SIGNATURES = {
     "fks_step_host": (c_int, [c_void_p, c_void_p, c_void_p, c_double]),
     "fks_step_bgk": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_double]),
     "fks_set_specular": (c_int, [c_void_p, c_int]),
+    "fks_set_scheme": (c_int, [c_void_p, c_int, c_int]),
     "fks_moments": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fks_get_state": (c_int, [c_void_p, ctypes.POINTER(c_int64), P_DOUBLE]),
     "fks_set_state": (c_int, [c_void_p, c_int64, c_double]),

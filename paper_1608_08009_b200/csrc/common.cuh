@@ -32,7 +32,9 @@ struct StepParams {
   const int* cell_list;      // fluid cells to process (local linear indices)
   int ncells;                // entries of cell_list
   int A;                     // directions (tables hold A + 1 entries, the last is the loss)
-  int mode;                  // 0 = collide (write Q), 1 = step (project + Euler)
+  int mode;                  // 0 = collide (write Q), 1 = step (project + Euler),
+                             // 2 = Heun stage: f_out = (f_base + f_in + dt/tau Pi Q(f_in)) / 2 (NEXT-4)
+  const double* f_base;      // mode 2: f* of the step [cells][n] (same cell indices as f_in)
   int project;               // apply a8
   double dt_tau;             // dt / tau
   double L, dv;              // velocity box half-width and spacing

@@ -266,6 +266,24 @@ void shift_delta(int64_t n, int N, double L, double dt, double h, int8_t* out) {
   }
 }
 
+// NEXT-4 (Strang, reading #26): delta between the half-step positions p and p + 1 (time p dt / 2):
+// s = floor(0.5 - (p * c) * 0.5); for even p this is bitwise the full-step s^{p/2} above.
+void shift_delta_half(int64_t p, int N, double L, double dt, double h, int8_t* out) {
+  const double dv = 2.0 * L / N;
+  for (int k = 0; k < N; ++k) {
+    volatile double v = -L + (k + 0.5) * dv;
+    volatile double vdt = v * dt;
+    volatile double c = vdt / h;
+    volatile double t0 = (double)p * c;
+    volatile double t1 = (double)(p + 1) * c;
+    volatile double h0 = t0 * 0.5;
+    volatile double h1 = t1 * 0.5;
+    volatile double a0 = 0.5 - h0;
+    volatile double a1 = 0.5 - h1;
+    out[k] = (int8_t)((int64_t)std::floor(a1) - (int64_t)std::floor(a0));
+  }
+}
+
 bool invert(std::vector<double> a, int m, double* out) {  // Gauss-Jordan with partial pivoting
   std::vector<double> b((size_t)m * m, 0.0);
   for (int i = 0; i < m; ++i) b[(size_t)i * m + i] = 1.0;
@@ -318,6 +336,9 @@ struct fks_ctx {
   int reflect = 0;  // NEXT-1: specular reflection at solid cells
   double* d_ghost[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   const double* halo[2] = {nullptr, nullptr};  // caller-owned neighbour planes (FKS_BC_HALO)
+  int split = FKS_SPLIT_LIE;       // NEXT-4 time scheme (fks_set_scheme)
+  int integ = FKS_TIME_EULER;
+  double* d_tmp = nullptr;         // one state-sized scratch for the Heun / Strang sequences
   double* d_host_in = nullptr;
   double* d_host_out = nullptr;
   // fks_step_host pipeline (0D, no solids): copy streams and per-chunk events
@@ -417,7 +438,7 @@ fks_status set_cell_lists(fks_ctx* c, const uint8_t* solid_host) {
 // Returns FKS_E_UNSUPPORTED when a shift along the slab axis exceeds one cell while that axis has a
 // HALO face: the neighbour rank sends exactly one plane (halo width 1 at CFL <= 1, reading #15), so a
 // source two planes away would silently read the wrong plane.
-fks_status fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift) {
+fks_status fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_shift, int64_t half = -1) {
   std::memset(tp, 0, sizeof(*tp));
   tp->dx = with_shift ? c->grid.dx : 0;
   for (int a = 0; a < 3; ++a) tp->M[a] = (int)c->grid.M[a];
@@ -425,7 +446,10 @@ fks_status fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_
   tp->halo[0] = c->halo[0];
   tp->halo[1] = c->halo[1];
   if (with_shift)
-    for (int a = 0; a < c->grid.dx; ++a) shift_delta(c->step_n, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
+    for (int a = 0; a < c->grid.dx; ++a) {
+      if (half >= 0) shift_delta_half(half, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
+      else shift_delta(c->step_n, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
+    }
   tp->solid = c->d_solid;
   tp->reflect = (c->reflect && c->d_solid && with_shift) ? 1 : 0;
   tp->Nv = c->N;
@@ -642,6 +666,18 @@ fks_status fks_set_solid(fks_ctx* c, const uint8_t* solid_host) {
   return set_cell_lists(c, solid_host);
 }
 
+fks_status fks_set_scheme(fks_ctx* c, int splitting, int integrator) {
+  if (!c || (splitting != FKS_SPLIT_LIE && splitting != FKS_SPLIT_STRANG) ||
+      (integrator != FKS_TIME_EULER && integrator != FKS_TIME_HEUN))
+    return FKS_E_INVAL;
+  if (splitting == FKS_SPLIT_STRANG)
+    for (int f = 0; f < 2 * c->grid.dx; ++f)
+      if (c->grid.bc[f] == FKS_BC_HALO) return FKS_E_UNSUPPORTED;
+  c->split = splitting;
+  c->integ = integrator;
+  return FKS_OK;
+}
+
 fks_status fks_set_stream(fks_ctx* c, void* s) {
   if (!c) return FKS_E_INVAL;
   c->stream = (cudaStream_t)s;
@@ -659,7 +695,9 @@ fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
 
 static fks_status check_dt(fks_ctx* c, double dt) {
   if (!(dt > 0)) return FKS_E_INVAL;
-  if (c->reflect)  // the neighbour rank's solid cells are not known here
+  if (c->reflect || (c->split == FKS_SPLIT_STRANG && c->grid.dx > 0))
+    // the neighbour rank's solid cells are not known here; Strang's second half transport would
+    // need a second exchange of the collided state
     for (int f = 0; f < 2 * c->grid.dx; ++f)
       if (c->grid.bc[f] == FKS_BC_HALO) return FKS_E_UNSUPPORTED;
   for (int f = 0; f < 2 * c->grid.dx; ++f) {
@@ -685,10 +723,82 @@ fks_status fks_transport(fks_ctx* c, const double* f_in, double* f_out, double d
   return FKS_OK;
 }
 
+static fks_status ensure_tmp(fks_ctx* c) {
+  if (c->d_tmp) return FKS_OK;
+  return cudaMalloc(&c->d_tmp, (size_t)c->ncells * c->n * sizeof(double)) == cudaSuccess ? FKS_OK : FKS_E_NOMEM;
+}
+
+// One collision pass over the fluid cells: mode 1 (f_out = f + dt/tau Pi Q(f)) or mode 2 (Heun stage,
+// f_out = (base + f + dt/tau Pi Q(f)) / 2) with the given transport (shifted or none).
+static fks_status collision_pass(fks_ctx* c, const double* in, double* out, int mode, const double* base,
+                                 const fks::TransportParams& tp) {
+  fks::StepParams p = base_params(c, in, out, mode);
+  p.tp = tp;
+  p.f_base = base;
+  p.cell_list = c->nsolid ? c->d_fluid : nullptr;
+  p.ncells = c->nfluid;
+  return run_collision(c, p);
+}
+
+static fks_status transport_pass(fks_ctx* c, const double* in, double* out, const fks::TransportParams& tp) {
+  cudaError_t e = fks::launch_transport(in, out, tp, c->d_solid, c->ncells, c->n, c->N, c->dv, c->stream);
+  c->launches++;
+  return cuda_fail(e);
+}
+
+static fks_status copy_solids(fks_ctx* c, const double* in, double* out) {
+  if (!c->nsolid) return FKS_OK;
+  cudaError_t e = fks::launch_copy_cells(in, out, c->d_solid_list, c->nsolid, c->n, c->stream);
+  c->launches++;
+  return cuda_fail(e);
+}
+
+// NEXT-4 step sequences (reading #26); all buffers distinct from f_in, the in-place passes are
+// collision passes without transport (each cell reads only its own vector before writing it).
+static fks_status step_scheme(fks_ctx* c, const double* f_in, double* f_out) {
+  fks_status st = ensure_tmp(c);
+  if (st != FKS_OK) return st;
+  double* tmp = c->d_tmp;
+  fks::TransportParams none, full, h1, h2;
+  fill_transport(c, &none, false);
+  const bool spatial = c->grid.dx > 0;
+  const bool strang = c->split == FKS_SPLIT_STRANG && spatial;
+  if (!strang) {  // Lie + Heun: f* = T f_in; f1 = E(f*); f_out = (f* + E(f1)) / 2
+    const double* fstar = f_in;
+    if (spatial) {
+      if ((st = fill_transport(c, &full, true)) != FKS_OK) return st;
+      if ((st = transport_pass(c, f_in, tmp, full)) != FKS_OK) return st;
+      fstar = tmp;
+    }
+    if ((st = copy_solids(c, f_in, f_out)) != FKS_OK) return st;
+    if ((st = collision_pass(c, fstar, f_out, 1, nullptr, none)) != FKS_OK) return st;
+    return collision_pass(c, f_out, f_out, 2, fstar, none);
+  }
+  if ((st = fill_transport(c, &h1, true, 2 * c->step_n)) != FKS_OK) return st;
+  if ((st = fill_transport(c, &h2, true, 2 * c->step_n + 1)) != FKS_OK) return st;
+  if (c->integ == FKS_TIME_EULER) {  // Strang + Euler: tmp = E(T_half f_in); f_out = T_half tmp
+    if ((st = copy_solids(c, f_in, tmp)) != FKS_OK) return st;
+    if ((st = collision_pass(c, f_in, tmp, 1, nullptr, h1)) != FKS_OK) return st;
+    return transport_pass(c, tmp, f_out, h2);
+  }
+  // Strang + Heun: f* = T_half f_in (in f_out); tmp = E(f*); tmp = (f* + E(tmp)) / 2; f_out = T_half tmp
+  if ((st = transport_pass(c, f_in, f_out, h1)) != FKS_OK) return st;
+  if ((st = copy_solids(c, f_in, tmp)) != FKS_OK) return st;
+  if ((st = collision_pass(c, f_out, tmp, 1, nullptr, none)) != FKS_OK) return st;
+  if ((st = collision_pass(c, tmp, tmp, 2, f_out, none)) != FKS_OK) return st;
+  return transport_pass(c, tmp, f_out, h2);
+}
+
 fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
+  if (c->integ != FKS_TIME_EULER || (c->split == FKS_SPLIT_STRANG && c->grid.dx > 0)) {
+    st = step_scheme(c, f_in, f_out);
+    if (st != FKS_OK) return st;
+    c->step_n++;
+    return FKS_OK;
+  }
   fks::StepParams p = base_params(c, f_in, f_out, 1);
   st = fill_transport(c, &p.tp, true);
   if (st != FKS_OK) return st;
@@ -708,19 +818,26 @@ fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
 fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt, int nu_rule, double mu) {
   if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
   if (nu_rule < FKS_NU_RHO || nu_rule > FKS_NU_EULER || (nu_rule == FKS_NU_CONST && !(mu > 0))) return FKS_E_INVAL;
+  if (c->integ != FKS_TIME_EULER) return FKS_E_UNSUPPORTED;  // the BGK step is forward Euler only
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
   fks::BgkParams p;
   std::memset(&p, 0, sizeof(p));
-  st = fill_transport(c, &p.tp, true);
-  if (st != FKS_OK) return st;
-  if (c->nsolid) {
-    if (fks::launch_copy_cells(f_in, f_out, c->d_solid_list, c->nsolid, c->n, c->stream) != cudaSuccess)
-      return FKS_E_CUDA;
-    c->launches++;
+  const bool strang = c->split == FKS_SPLIT_STRANG && c->grid.dx > 0;  // NEXT-4: T_half B T_half
+  double* out1 = f_out;
+  fks::TransportParams h2;
+  if (strang) {
+    if ((st = ensure_tmp(c)) != FKS_OK) return st;
+    out1 = c->d_tmp;
+    if ((st = fill_transport(c, &p.tp, true, 2 * c->step_n)) != FKS_OK) return st;
+    if ((st = fill_transport(c, &h2, true, 2 * c->step_n + 1)) != FKS_OK) return st;
+  } else {
+    st = fill_transport(c, &p.tp, true);
+    if (st != FKS_OK) return st;
   }
+  if ((st = copy_solids(c, f_in, out1)) != FKS_OK) return st;
   p.f_in = f_in;
-  p.f_out = f_out;
+  p.f_out = out1;
   p.nonfinite = c->d_flag;
   p.cell_list = c->nsolid ? c->d_fluid : nullptr;
   p.ncells = c->nfluid;
@@ -733,6 +850,7 @@ fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt
   cudaError_t e = fks::launch_bgk(c->N, c->dv, p, c->sm_count, c->stream);
   c->launches++;
   if (e != cudaSuccess) return FKS_E_CUDA;
+  if (strang && (st = transport_pass(c, out1, f_out, h2)) != FKS_OK) return st;
   c->step_n++;
   return FKS_OK;
 }
@@ -807,7 +925,8 @@ fks_status fks_step_host(fks_ctx* c, const double* f_in_host, double* f_out_host
     c->d_host_in = in;
     c->d_host_out = out;
   }
-  if (c->grid.dx == 0 && c->nsolid == 0) return step_host_pipelined(c, f_in_host, f_out_host, dt);
+  if (c->grid.dx == 0 && c->nsolid == 0 && c->integ == FKS_TIME_EULER)
+    return step_host_pipelined(c, f_in_host, f_out_host, dt);
   if (cudaMemcpyAsync(c->d_host_in, f_in_host, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     return FKS_E_CUDA;
   fks_status st = fks_step(c, c->d_host_in, c->d_host_out, dt);
@@ -868,6 +987,7 @@ fks_status fks_finalize(fks_ctx* c) {
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   cudaFree(c->d_host_in);
   cudaFree(c->d_host_out);
+  cudaFree(c->d_tmp);
   delete c;
   return FKS_OK;
 }

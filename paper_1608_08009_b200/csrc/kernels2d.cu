@@ -301,10 +301,12 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
       }
     }
     bool bad = false;
+    const double* hbase = p.mode == 2 ? p.f_base + cell * (int64_t)n : nullptr;
     auto euler = [&](int x, double fs) {
       const double vx = node_v(x, p.L, p.dv);
       const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * (vx * vx + vy * vy);
-      const double o = fma(p.dt_tau, q[x] - corr, fs);
+      double o = fma(p.dt_tau, q[x] - corr, fs);
+      if (hbase) o = 0.5 * (o + __ldcs(hbase + x + N * tx));  // Heun: (f* + E(f1)) / 2 (NEXT-4)
       bad |= !isfinite(o);
       if (active) out[x + N * tx] = o;
     };

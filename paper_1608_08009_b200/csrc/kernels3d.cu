@@ -730,11 +730,13 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
         for (int a = 0; a < 5; ++a) lam[a] = c.part[a];
       }
       bool bad = false;
+      const double* base = p.mode == 2 ? p.f_base + cell * (int64_t)n : nullptr;
       auto euler = [&](int y, double fs) {
         const double vy = node_v(y, p.L, p.dv);
         const int k = tx + N * (y + N * z);
         const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * vz + lam[4] * (vx * vx + vy * vy + vz * vz);
-        const double o = fma(p.dt_tau, q[y] - corr, fs);
+        double o = fma(p.dt_tau, q[y] - corr, fs);
+        if (base) o = 0.5 * (o + __ldcs(base + k));  // Heun: (f* + E(f1)) / 2 (NEXT-4)
         bad |= !isfinite(o);
         out[k] = o;
       };

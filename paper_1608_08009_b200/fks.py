@@ -12,6 +12,8 @@ from ._lib import FksError, FksGrid, check, load  # noqa: F401
 
 BC_PERIODIC, BC_GHOST, BC_OUTFLOW, BC_HALO = 0, 1, 2, 3
 NU_RHO, NU_CONST, NU_EULER = 0, 1, 2  # fks_step_bgk collision-frequency rules (include/fks.h)
+SPLIT_LIE, SPLIT_STRANG = 0, 1         # fks_set_scheme (NEXT-4)
+TIME_EULER, TIME_HEUN = 0, 1
 
 
 def _ptr(t):
@@ -85,6 +87,10 @@ class Context:
     def set_specular(self, on=True):
         """NEXT-1: specular reflection at solid cells (fks_set_specular)."""
         check(self._lib.fks_set_specular(self.handle, int(bool(on))), "fks_set_specular")
+
+    def set_scheme(self, splitting=SPLIT_LIE, integrator=TIME_EULER):
+        """NEXT-4: splitting SPLIT_LIE / SPLIT_STRANG, integrator TIME_EULER / TIME_HEUN (fks_set_scheme)."""
+        check(self._lib.fks_set_scheme(self.handle, int(splitting), int(integrator)), "fks_set_scheme")
 
     def set_stream(self, stream):
         """stream: a torch.cuda.Stream (or None for the default stream)."""

@@ -99,3 +99,165 @@ def test_step_3d_maxwell_molecules_C2_cells(torch, fks):
     got = host(out)
     for i in range(nc):
         assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
+# ---------------------------------------------------------------- NEXT-4: Heun and Strang
+from oracle import bgk, transport  # noqa: E402
+
+
+def _spatial(dxd, dv, M, N, L, bc, seed):
+    rng = np.random.default_rng(300 + seed)
+    h = 0.1
+    dt = 0.93 * h / (L - L / N)
+    shape = tuple(M[::-1]) + (N,) * dv
+    base = workloads.family("smooth", dv, N, L, 1, seed=seed)[0]
+    F = (base[None] * rng.uniform(0.5, 1.5, int(np.prod(M)))[(...,) + (None,) * dv]).reshape(shape)
+    ghosts = {f: workloads.family("smooth", dv, N, L, 1, seed=seed + 10 + f)[0] for f in range(2 * dxd)
+              if bc[f] == transport.GHOST}
+    return F, h, dt, ghosts
+
+
+@pytest.mark.parametrize("dv,N,L,A,nc", [(3, 32, 7.0, 24, 5), (2, 32, 9.0, 8, 37), (3, 16, 7.0, 24, 9)])
+def test_heun_0d(torch, fks, dv, N, L, A, nc):
+    """Heun (RK2) collision integrator on homogeneous cells, three steps, vs the oracle."""
+    f = workloads.family("smooth" if dv == 3 else "bkw", dv, N, L, nc, seed=61)
+    ctx = fks.Context(dv, 0, [nc], N, L, A)
+    ctx.set_params(tau=0.7)
+    ctx.set_scheme(fks.SPLIT_LIE, fks.TIME_HEUN)
+    a, b = dev(torch, f), torch.empty_like(dev(torch, f))
+    tab = tables.build_tables(dv, N, L, A=A) if dv == 2 else tables.build_tables(3, N, L)
+    ref = f.copy()
+    for _ in range(3):
+        ctx.step(a, b, 0.05)
+        a, b = b, a
+        ref = ostep.homogeneous_step(ref, tab, 0.05, tau=0.7, integrator="heun")
+    ctx.check()
+    got = host(a)
+    for i in range(nc):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
+@pytest.mark.parametrize("split,integ", [("lie", "heun"), ("strang", "euler"), ("strang", "heun")])
+@pytest.mark.parametrize("dxd,dv,M,N,bc,specular", [
+    (1, 3, [9], 8, [transport.GHOST, transport.OUTFLOW], False),
+    (2, 2, [6, 5], 16, [transport.GHOST, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC], False),
+    (2, 3, [5, 4], 8, [transport.GHOST, transport.OUTFLOW, transport.OUTFLOW, transport.OUTFLOW], True),
+    (3, 3, [3, 3, 3], 8, [transport.PERIODIC] * 2 + [transport.OUTFLOW, transport.GHOST] + [transport.PERIODIC] * 2,
+     False),
+])
+def test_scheme_with_transport(torch, fks, dxd, dv, M, N, bc, specular, split, integ):
+    """fks_set_scheme sequences (reading #26) with every face kind, solids and specular walls, three
+    steps against the oracle's step(splitting=..., integrator=...)."""
+    L = 6.0
+    F, h, dt, ghosts = _spatial(dxd, dv, M, N, L, bc, seed=dxd * 3 + dv)
+    solid = np.zeros(tuple(M[::-1]), dtype=bool)
+    solid.reshape(-1)[int(np.prod(M)) // 2] = True
+    A = 8 if dv == 2 else 24
+    ctx = fks.Context(dv, dxd, M, N, L, A, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_solid(solid)
+    if specular:
+        ctx.set_specular(True)
+    ctx.set_params(tau=0.4)
+    ctx.set_scheme(fks.SPLIT_STRANG if split == "strang" else fks.SPLIT_LIE,
+                   fks.TIME_HEUN if integ == "heun" else fks.TIME_EULER)
+    tab = tables.build_tables(dv, N, L, A=8) if dv == 2 else tables.build_tables(dv, N, L)
+    cfg = dict(dx_dim=dxd, dv=dv, N=N, L=L, dt=dt, dx=h, tau=0.4, bc=bc, ghosts=ghosts, solid=solid,
+               specular=specular)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(3):
+        ctx.step(a, b, dt)
+        a, b = b, a
+        ref = ostep.step(ref, s, cfg, tab, integrator=integ, splitting=split)
+    ctx.check()
+    got = host(a).reshape((-1,) + (N,) * dv)
+    ref = ref.reshape((-1,) + (N,) * dv)
+    for i in range(ref.shape[0]):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i])), i
+
+
+def test_strang_bgk(torch, fks):
+    """Strang splitting of the BGK step (NEXT-2 x NEXT-4): T_half B T_half vs the oracle."""
+    dxd, dv, M, N, L = 2, 2, [6, 5], 16, 6.0
+    bc = [transport.GHOST, transport.OUTFLOW, transport.PERIODIC, transport.PERIODIC]
+    F, h, dt, ghosts = _spatial(dxd, dv, M, N, L, bc, seed=5)
+    ctx = fks.Context(dv, dxd, M, N, L, 8, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_params(tau=0.5)
+    ctx.set_scheme(fks.SPLIT_STRANG, fks.TIME_EULER)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(2):
+        ctx.step_bgk(a, b, dt, bgk.NU_RHO, 0.0)
+        a, b = b, a
+        d1 = transport.shift_delta_half(2 * s, N, L, dt, h)
+        d2 = transport.shift_delta_half(2 * s + 1, N, L, dt, h)
+        fs = transport.gather(ref, s, dxd, dv, N, L, dt, h, bc, ghosts, delta=d1)
+        mid = np.empty_like(fs)
+        for j in range(int(np.prod(M))):
+            idx = np.unravel_index(j, tuple(M[::-1]))
+            mid[idx] = bgk.bgk_step_cell(fs[idx], dt, 0.5, bgk.NU_RHO, 0.0, dv, N, L)
+        ref = transport.gather(mid, s, dxd, dv, N, L, dt, h, bc, ghosts, delta=d2)
+    got = host(a).reshape((-1,) + (N,) * dv)
+    ref = ref.reshape((-1,) + (N,) * dv)
+    for i in range(ref.shape[0]):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
+def test_scheme_argument_errors(torch, fks):
+    """fks_set_scheme validates its arguments; Strang is refused on a partitioned grid and Heun by
+    the BGK step (include/fks.h)."""
+    N, L = 8, 7.0
+    ctx = fks.Context(3, 0, [2], N, L, 24)
+    for sp, it in ((2, 0), (0, 5), (-1, 0)):
+        with pytest.raises(fks.FksError) as ei:
+            ctx.set_scheme(sp, it)
+        assert ei.value.status == -1
+    ctx.set_scheme(fks.SPLIT_LIE, fks.TIME_HEUN)
+    f = dev(torch, workloads.family("smooth", 3, N, L, 2, seed=6))
+    with pytest.raises(fks.FksError) as ei:
+        ctx.step_bgk(f, torch.empty_like(f), 0.01, bgk.NU_RHO, 0.0)
+    assert ei.value.status == -2
+    ctx2 = fks.Context(3, 1, [4], N, L, 24, h=0.1, bc=[fks.BC_HALO, fks.BC_OUTFLOW])
+    with pytest.raises(fks.FksError) as ei:
+        ctx2.set_scheme(fks.SPLIT_STRANG, fks.TIME_EULER)
+    assert ei.value.status == -2
+    ctx2.set_scheme(fks.SPLIT_LIE, fks.TIME_HEUN)   # Heun on a partitioned grid is fine
+
+
+def test_full_size_C3_strang_heun_sampled(torch, fks):
+    """BASELINE configs[2] (1Dx3D Sod, 400 cells, Dirichlet ghosts, 32^3) at full size with Strang
+    splitting + Heun: one step, sampled cells (both faces, the contact, the interior) against the
+    oracle, which computes the collided half-step state only where the second half transport reads."""
+    c = workloads.config("C3")
+    N, L, A, dv, dxd = c["N"], c["L"], c["A"], c["dv"], c["dx_dim"]
+    M = list(c["cells"][::-1])
+    F = workloads.initial_state(c)
+    F = F * (1.0 + 0.1 * np.random.default_rng(12).random(F.shape[:1]))[(...,) + (None,) * dv]
+    ghosts = workloads.ghost_vectors(c)
+    ctx = fks.Context(dv, dxd, M, N, L, A, h=c["dx"], bc=c["bc"])
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_params(tau=c["tau"])
+    ctx.set_scheme(fks.SPLIT_STRANG, fks.TIME_HEUN)
+    out = torch.empty_like(dev(torch, F))
+    ctx.step(dev(torch, F), out, c["dt"])
+    ctx.check()
+    got = host(out)
+    sample = [0, 1, 199, 200, 201, 398, 399]
+    need = sorted({j + d for j in sample for d in (-1, 0, 1) if 0 <= j + d < M[0]})
+    dt, hx = c["dt"], c["dx"]
+    d1 = transport.shift_delta_half(0, N, L, dt, hx)
+    d2 = transport.shift_delta_half(1, N, L, dt, hx)
+    fs = transport.gather(F, 0, dxd, dv, N, L, dt, hx, c["bc"], ghosts, cells=need, delta=d1)
+    tab = tables.build_tables(dv, N, L)
+    cfg = dict(dv=dv, N=N, L=L, dt=dt, tau=c["tau"])
+    mid = np.full_like(F, np.nan)
+    for i, j in enumerate(need):
+        mid[j] = ostep._collision_update(fs[i], cfg, tab, collision.collide_fft, "heun")
+    ref = transport.gather(mid, 0, dxd, dv, N, L, dt, hx, c["bc"], ghosts, cells=sample, delta=d2)
+    for i, j in enumerate(sample):
+        assert np.max(np.abs(got[j] - ref[i])) <= TOL * np.max(np.abs(ref[i])), j
