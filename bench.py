@@ -35,17 +35,35 @@ def hbm_peak():
         return 7700.0
 
 
-def dram_traffic(dv, ncells):
+def dram_traffic(dv, ncells, config=None):
     """dram__bytes_read + dram__bytes_write per launch from the committed `ncu --set full` capture
-    of the dominant kernel (per-cell figure x cells of this launch), or None."""
-    path = NCU_SUMMARY.get(dv)
-    if not path or not os.path.exists(path):
-        return None
-    with open(path) as fh:
-        return json.load(fh)["dram_bytes_per_cell"] * ncells
-# FP64 DFMA peak derived from unit counts and clocks (B200_PROFILING.md: 148 SMs, 1965 MHz max;
-# 64 DFMA/clk/SM), measured 37.1 TFLOP/s in profiles/r01_microbench.txt.
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+    of the dominant kernel on this config (profiles/r02_ncu_<kernel>_<config>.json: per-cell figure x
+    cells of this launch), else the round-1 capture, else None.  Returns (bytes, source)."""
+    kern = "k_step3d" if dv == 3 else "k_step2d"
+    paths = ([os.path.join(ROOT, "profiles", f"r02_ncu_{kern}_{config}.json")] if config else []) + [NCU_SUMMARY.get(dv)]
+    for path in paths:
+        if path and os.path.exists(path):
+            with open(path) as fh:
+                return json.load(fh)["dram_bytes_per_cell"] * ncells, os.path.relpath(path, ROOT)
+    return None, None
+# FP64 DFMA peak: the SUSTAINED measurement committed in profiles/r02_peaks.json (>= 8 s of DFMA
+# back to back on this pool's B200, clocks logged; tools/microbench/mb_dsmem.cu), else the figure
+# derived from unit counts and clocks (B200_PROFILING.md: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz).
+FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+PEAKS_R02 = os.path.join(ROOT, "profiles", "r02_peaks.json")
+
+
+def fp64_peak():
+    """(TFLOP/s, source) of the FP64 roofline denominator."""
+    try:
+        with open(PEAKS_R02) as fh:
+            d = json.load(fh)
+        return float(d["fp64_tflops_sustained"]), d.get("fp64_source", os.path.relpath(PEAKS_R02, ROOT))
+    except (OSError, KeyError, ValueError):
+        return FP64_PEAK_DERIVED, "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"
+
+
+FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = fp64_peak()
 
 
 def flops_per_cell(dv, N, A):
@@ -64,6 +82,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-spatial-secondary", action="store_true", help="skip the C4 fused-step secondary figure")
     return ap.parse_args()
 
 
@@ -121,6 +140,24 @@ def _oracle_worker(args):
     return time.perf_counter() - t0
 
 
+def direct_timing():
+    """the oracle's literal O(n^2 (A+1)) bilinear form (the paper's "naive" evaluation,
+    P:414) timed on one 2D 32^2 cell (A = 8) and one 3D 16^3 cell (A = 24), single core; the 3D 32^3
+    figure is extrapolated by (32768 / 4096)^2 = 64 (the cost is n^2 (A+1) complex MACs)."""
+    import numpy as np
+    import workloads
+    from oracle import collision, tables
+    out = {}
+    for dv, N, L, A in ((2, 32, 9.0, 8), (3, 16, 7.0, 24)):
+        f = workloads.family("smooth", dv, N, L, 1, seed=1)[0]
+        tab = tables.build_tables(dv, N, L, A=A) if dv == 2 else tables.build_tables(3, N, L)
+        t0 = time.perf_counter()
+        collision.collide_direct(f, tab)
+        out[f"direct_{dv}d_{N}_s_per_cell"] = time.perf_counter() - t0
+    out["direct_3d_32_s_per_cell_extrapolated"] = out["direct_3d_16_s_per_cell"] * 64
+    return out
+
+
 def oracle_rate(name, seconds=15.0, cores=None):
     """cells/s of the oracle's fast evaluator (collide_fft + projection + Euler, numpy) over a
     bounded sample, one single-threaded worker per host core."""
@@ -138,6 +175,60 @@ def oracle_rate(name, seconds=15.0, cores=None):
                                            "fft") for i in range(cores)])
     wall = max(times)  # workers run concurrently; each times only its own step loop
     return tot / wall, cores, tot, wall
+
+
+def spatial_secondary(name, stream, reps):
+    """The transport-fused path on a spatial config (default: C4, 2Dx3D 100^2 cells with the solid
+    boxes, inflow/outflow): fks_step (a1..a9 fused, ghosts, solids) timed with CUDA events, plus
+    fks_transport alone (HBM-bound)."""
+    import numpy as np
+    import torch
+    import workloads
+    from paper_1608_08009_b200 import fks
+    c = workloads.config(name)
+    dv, N, A = c["dv"], c["N"], c["A"]
+    n = N ** dv
+    M = list(c["cells"][::-1])
+    nc = int(np.prod(M))
+    ctx = fks.Context(dv, c["dx_dim"], M, N, c["L"], A, h=c["dx"], bc=c["bc"])
+    for face, g in workloads.ghost_vectors(c).items():
+        ctx.set_ghost(face, torch.from_numpy(g).cuda())
+    solid = workloads.solid_mask(c)
+    nfl = nc
+    if solid is not None:
+        ctx.set_solid(solid)
+        nfl = nc - int(solid.sum())
+    ctx.set_params(tau=c["tau"])
+    ctx.set_stream(stream)
+    v = torch.from_numpy(workloads.initial_state(c, ncells=1).reshape(-1)[:n].copy()).cuda()
+    s = torch.from_numpy(1.0 + 0.1 * np.random.default_rng(1).random(nc)).cuda()
+    fa = (v[None, :] * s[:, None]).contiguous()
+    fb = torch.empty_like(fa)
+    dt = c["dt"]
+
+    def timed(fn, k):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / k
+    ms = timed(lambda: ctx.step(fa, fb, dt), reps)
+    ms_t = timed(lambda: ctx.transport(fa, fb, dt), reps)
+    ctx.check()
+    ach = flops_per_cell(dv, N, A) * nfl / (ms * 1e-3) / 1e12
+    gbs = 2 * nc * n * 8 / (ms_t * 1e-3) / 1e9
+    ctx.close()
+    del fa, fb
+    torch.cuda.empty_cache()
+    return {"value": nfl / (ms * 1e-3), "unit": "cells/s", "ms": ms, "fp64_frac": ach / FP64_PEAK_TFLOPS,
+            "phase_space_updates_per_s": nfl * n / (ms * 1e-3),
+            "transport_only": {"ms": ms_t, "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak()},
+            "what": f"{name} fks_step fused with FKS transport (ghost inflow, outflow, {nc - nfl} solid cells), "
+                    f"{nfl} fluid cells, {reps} steps; transport_only = fks_transport alone (16 B per update)"}
 
 
 # ------------------------------------------------------------------ main
@@ -222,7 +313,9 @@ def main():
             v = torch.from_numpy(workloads.initial_state(c, ncells=1).reshape(-1)[:n].copy()).cuda()
             fa = v.expand(int(np.prod(slab.M_local)), n).contiguous()
             F = None
-        stepper = parallel.DistributedStep(ctx, slab, n, torch.device("cuda", local)) if world > 1 else None
+        if world > 1:  # a2 inside libfks: NCCL communicator of the library, crossing slices only
+            parallel.init_libfks_comm(ctx, rank, world)
+        stepper = None
         scaling = "strong"
         ncells = int(np.prod(slab.M_local))
     ctx.set_params(tau=c["tau"])
@@ -344,6 +437,8 @@ def main():
                                  "hbm_frac": gbs / hbm_peak(),
                                  "what": "fks_moments (a10, 8 B read per phase-space point), HBM-bound"}
         ctx.check()
+        if c["dx_dim"] == 0 and dv == 3 and not a.no_spatial_secondary:
+            extra["C4_fused_step"] = spatial_secondary("C4", stream, reps)
 
     # ---- e2e through the C ABI with host buffers (H2D + step + D2H per step) --------------
     e2e = None
@@ -378,6 +473,7 @@ def main():
                "d2h_bytes_per_step": bytes_, "steps": ksteps, "path": "fks_step_host (pinned host buffers)"}
         ctx_h.close()
 
+    traffic, traffic_src = dram_traffic(dv, nfluid_local, a.config)
     if rank == 0:
         cpu = None
         if not a.no_cpu_baseline and world == 1:
@@ -385,6 +481,10 @@ def main():
             cpu = {"value": rate, "unit": "cells/s", "cores": cores, "kind": "oracle",
                    "sample": f"{tot} cells of {a.config} (oracle collide_fft + projection + Euler, numpy fp64) "
                              f"in {wall:.1f} s on {cores} single-threaded processes"}
+            try:
+                cpu["direct"] = direct_timing()
+            except MemoryError:
+                cpu["direct"] = None
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
@@ -405,15 +505,15 @@ def main():
                                 f"{world} slabs along space axis {c['dx_dim'] - 1}, NCCL halo exchange per step")},
             "phase_space_updates_per_s": value * n,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": dram_traffic(dv, ncells),
-                         "traffic_unit": "bytes per launch (ncu dram read+write per cell x cells, "
-                                         f"{os.path.relpath(NCU_SUMMARY[dv], ROOT)})",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "traffic_unit": f"bytes per launch (ncu dram read+write per cell x cells, {traffic_src})",
+                         "peak_source": FP64_PEAK_SOURCE,
                          "algorithmic_bytes": 2 * n * 8 * ncells,
                          "hbm_frac": (2 * n * 8 * nfluid_local / (kern_avg_ms * 1e-3) / 1e9) / hbm_peak(),
                          "kernel": "k_step3d" if dv == 3 else "k_step2d",
                          "flops_per_cell": fl, "kernel_ms_avg": kern_avg_ms,
-                         "note": "FP64 DFMA peak 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured 37.1); "
-                                 "flops in the 5 n log2 n FFT convention (SURVEY App. A.9)"},
+                         "note": "flops in the 5 n log2 n FFT convention (SURVEY App. A.9); the peak is the "
+                                 "sustained DFMA measurement when profiles/r02_peaks.json holds one"},
             "gpu_launches": launches,
             "secondary": extra,
             "clocks": clk,

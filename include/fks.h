@@ -40,6 +40,7 @@ extern "C" {
 #endif
 
 typedef struct fks_ctx fks_ctx;
+typedef struct fks_loopback fks_loopback;  /* in-process communicator (tests on one device) */
 
 typedef enum {
   FKS_OK = 0,
@@ -102,6 +103,38 @@ fks_status fks_set_ghost(fks_ctx* ctx, int face, const double* ghost_f);
  * slowest axis, cells in C order over the other axes).  The pointers are used by the next
  * fks_step / fks_transport calls (not copied); NULL for a face without a HALO. */
 fks_status fks_set_halo(fks_ctx* ctx, const double* lo_plane, const double* hi_plane);
+
+/* a2 inside the library: the slab halo exchange of the paper's MPI z-slab decomposition
+ * (Fig. mpi-decomp; ghost cells exchanged every step) over NCCL (NVLink /
+ * NVSwitch between the GPUs of a box), one rank per GPU.  The slab axis is the slowest space axis
+ * (dx - 1); its HALO faces name the neighbours: lo face -> rank - 1, hi face -> rank + 1 (mod nranks,
+ * so a periodic global axis is a ring).  Per step only the velocity slices whose FKS shift crosses
+ * the face are sent (k_a with delta = +1 to the lower rank, -1 to the upper one; halo width 1 at
+ * CFL <= 1), packed on a library communication stream, exchanged with grouped ncclSend/ncclRecv and
+ * unpacked into library-owned neighbour planes; fks_step runs the interior cells while the exchange
+ * is in flight and the cells of the HALO-face planes after it.  fks_transport and fks_step_bgk use
+ * the same exchange (before their kernel).  A comm replaces fks_set_halo.
+ *
+ * fks_comm_unique_id: a new NCCL unique id (128 bytes) -- call on one rank, broadcast the bytes
+ *   (e.g. torch.distributed), then every rank calls fks_set_comm with it.  NCCL is loaded at run
+ *   time (dlopen libnccl.so.2, reusing an already loaded copy); FKS_E_NCCL if unavailable or an
+ *   NCCL call fails.
+ * fks_set_comm: build this rank's communicator (collective over the nranks processes).  dx >= 1;
+ *   FKS_E_UNSUPPORTED with specular reflection; once per context.
+ * fks_comm_loopback_create / fks_set_comm_loopback: the same exchange between contexts of ONE
+ *   process through device copies (all ranks on one GPU, driven in turn): every rank must call
+ *   fks_halo_post for the step before any rank steps (FKS_E_STATE otherwise).
+ * fks_halo_post: pack and send this step's planes of f_in now (optional with NCCL: fks_step posts
+ *   for itself); dt must already be fixed (a first step or fks_set_state), else FKS_E_STATE.
+ * fks_get_comm_stats: payload bytes sent by the last exchange (both faces), and the fluid cells run
+ *   before / after the exchange completes. */
+fks_status fks_comm_unique_id(void* nccl_unique_id_out);
+fks_status fks_set_comm(fks_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
+fks_status fks_comm_loopback_create(int nranks, fks_loopback** out);
+fks_status fks_comm_loopback_destroy(fks_loopback* loop);
+fks_status fks_set_comm_loopback(fks_ctx* ctx, fks_loopback* loop, int rank);
+fks_status fks_halo_post(fks_ctx* ctx, const double* f_in);
+fks_status fks_get_comm_stats(const fks_ctx* ctx, int64_t* bytes_sent_last, int* interior_cells, int* boundary_cells);
 
 /* Solid mask (host, one byte per local cell, copied): solid cells are not collided and keep
  * their values (reading #19; specular reflection is NEXT work). NULL clears it. */
@@ -187,6 +220,12 @@ const char* fks_strerror(fks_status s);
 fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, double kernel_const,
                            double kernel_gamma, double* alpha_host, double* alphap_host, double* D_host,
                            double* w_host, double* e_host, double* scale);
+
+/* a2 plan of step n: the velocity indices k (along the slab axis) whose slices the exchange sends to
+ * the lower rank (delta = +1) and to the upper rank (delta = -1); arrays of Nv entries.
+ * FKS_E_UNSUPPORTED if some |delta| > 1 (halo width 1). */
+fks_status fks_host_halo_slices(int64_t n, int Nv, double L, double dt, double h, int8_t* to_lower, int* n_lower,
+                                int8_t* to_upper, int* n_upper);
 
 /* delta_k = s^{n+1}_k - s^n_k for the N nodes of one velocity axis (a1). */
 fks_status fks_host_shift(int64_t n, int Nv, double L, double dt, double h, int8_t* delta_host);

@@ -32,6 +32,13 @@ SIGNATURES = {
     "fks_step_bgk": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_double]),
     "fks_set_specular": (c_int, [c_void_p, c_int]),
     "fks_set_scheme": (c_int, [c_void_p, c_int, c_int]),
+    "fks_comm_unique_id": (c_int, [c_void_p]),
+    "fks_set_comm": (c_int, [c_void_p, c_void_p, c_int, c_int]),
+    "fks_comm_loopback_create": (c_int, [c_int, ctypes.POINTER(c_void_p)]),
+    "fks_comm_loopback_destroy": (c_int, [c_void_p]),
+    "fks_set_comm_loopback": (c_int, [c_void_p, c_void_p, c_int]),
+    "fks_halo_post": (c_int, [c_void_p, c_void_p]),
+    "fks_get_comm_stats": (c_int, [c_void_p, ctypes.POINTER(c_int64), ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "fks_moments": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fks_get_state": (c_int, [c_void_p, ctypes.POINTER(c_int64), P_DOUBLE]),
     "fks_set_state": (c_int, [c_void_p, c_int64, c_double]),
@@ -42,6 +49,8 @@ SIGNATURES = {
     "fks_host_tables": (c_int, [c_int, c_int, c_double, c_int, c_double, c_double, c_double, P_DOUBLE, P_DOUBLE,
                                 P_DOUBLE, P_DOUBLE, P_DOUBLE, P_DOUBLE]),
     "fks_host_shift": (c_int, [c_int64, c_int, c_double, c_double, c_double, ctypes.POINTER(ctypes.c_int8)]),
+    "fks_host_halo_slices": (c_int, [c_int64, c_int, c_double, c_double, c_double, ctypes.POINTER(ctypes.c_int8),
+                                     ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_int8), ctypes.POINTER(c_int)]),
 }
 
 _lib = None

@@ -3,6 +3,8 @@
 // Compiled with -fmad=false / -ffp-contract=off for the host so the shift formula rounds
 // exactly as stated in DESIGN.md reading #16.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is dlopen'ed by fks_set_comm (no link-time dependency)
 
 #include <algorithm>
 #include <cmath>
@@ -345,6 +347,35 @@ struct fks_ctx {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
   int64_t launches = 0;
+  // a2 inside the library (fks_set_comm / fks_set_comm_loopback): per HALO face f (0 = lo, 1 = hi of
+  // the slab axis) a library-owned neighbour plane [pc][n], packed send / receive buffers holding only
+  // the velocity slices whose shift crosses that face this step, a communication stream and events.
+  int comm_kind = 0;               // 0 none, 1 NCCL, 2 loopback
+  ncclComm_t nccl = nullptr;
+  fks_loopback* loop = nullptr;
+  int rank = 0, nranks = 1;
+  int peer[2] = {-1, -1};          // neighbour rank across the lo / hi face (-1: not a HALO face)
+  cudaStream_t s_comm = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr, ev_packed = nullptr;
+  double* d_halo[2] = {nullptr, nullptr};
+  double* d_send[2] = {nullptr, nullptr};
+  double* d_recv[2] = {nullptr, nullptr};
+  fks::SliceList send_sl[2], recv_sl[2];
+  int64_t pc = 0;                  // cells per plane of the slab axis
+  int64_t posted = -1;             // step whose exchange has been posted
+  int64_t bytes_sent = 0;          // payload sent by the last exchange (both faces)
+  int* d_interior = nullptr;       // fluid cells that never read a halo plane
+  int ninterior = 0;
+  int* d_boundary = nullptr;       // fluid cells on a HALO-face plane
+  int nboundary = 0;
+  std::vector<uint8_t> h_solid;    // host copy of the solid mask (empty: none)
+};
+
+// Loopback communicator: contexts of one process (one device) exchange through device copies,
+// so a partitioned run can be checked on one GPU (fks_comm_loopback_create).
+struct fks_loopback {
+  int nranks = 0;
+  std::vector<fks_ctx*> ctx;
 };
 
 namespace {
@@ -413,7 +444,11 @@ void build_gram(fks_ctx* c) {
   invert(g, m, c->Ginv);
 }
 
+fks_status update_comm_lists(fks_ctx* c);
+
 fks_status set_cell_lists(fks_ctx* c, const uint8_t* solid_host) {
+  if (solid_host) c->h_solid.assign(solid_host, solid_host + c->ncells);
+  else c->h_solid.clear();
   std::vector<int> fluid, solid;
   for (int64_t i = 0; i < c->ncells; ++i) {
     if (solid_host && solid_host[i]) solid.push_back((int)i); else fluid.push_back((int)i);
@@ -432,7 +467,38 @@ fks_status set_cell_lists(fks_ctx* c, const uint8_t* solid_host) {
     if (cudaMalloc(&c->d_solid, c->ncells) != cudaSuccess) return FKS_E_NOMEM;
     cudaMemcpy(c->d_solid, solid_host, c->ncells, cudaMemcpyHostToDevice);
   }
+  fks_status st = update_comm_lists(c);
+  if (st != FKS_OK) return st;
   return cuda_fail(cudaGetLastError());
+}
+
+// a2: fluid cells split into those on a HALO-face plane of the slab axis (they may read a neighbour
+// plane, CFL <= 1) and the interior, so the interior runs while the exchange is in flight.
+fks_status update_comm_lists(fks_ctx* c) {
+  cudaFree(c->d_interior); cudaFree(c->d_boundary);
+  c->d_interior = c->d_boundary = nullptr;
+  c->ninterior = c->nboundary = 0;
+  if (c->comm_kind == 0) return FKS_OK;
+  const int a = c->grid.dx - 1;
+  const int64_t Ma = c->grid.M[a];
+  std::vector<int> in, bd;
+  for (int64_t i = 0; i < c->ncells; ++i) {
+    if (!c->h_solid.empty() && c->h_solid[i]) continue;
+    const int64_t ja = i / c->pc;  // slab axis = slowest axis
+    const bool edge = (c->peer[0] >= 0 && ja == 0) || (c->peer[1] >= 0 && ja == Ma - 1);
+    (edge ? bd : in).push_back((int)i);
+  }
+  c->ninterior = (int)in.size();
+  c->nboundary = (int)bd.size();
+  if (!in.empty()) {
+    if (cudaMalloc(&c->d_interior, in.size() * sizeof(int)) != cudaSuccess) return FKS_E_NOMEM;
+    cudaMemcpy(c->d_interior, in.data(), in.size() * sizeof(int), cudaMemcpyHostToDevice);
+  }
+  if (!bd.empty()) {
+    if (cudaMalloc(&c->d_boundary, bd.size() * sizeof(int)) != cudaSuccess) return FKS_E_NOMEM;
+    cudaMemcpy(c->d_boundary, bd.data(), bd.size() * sizeof(int), cudaMemcpyHostToDevice);
+  }
+  return FKS_OK;
 }
 
 // Returns FKS_E_UNSUPPORTED when a shift along the slab axis exceeds one cell while that axis has a
@@ -443,8 +509,8 @@ fks_status fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_
   tp->dx = with_shift ? c->grid.dx : 0;
   for (int a = 0; a < 3; ++a) tp->M[a] = (int)c->grid.M[a];
   for (int f = 0; f < 6; ++f) { tp->bc[f] = c->grid.bc[f]; tp->ghost[f] = c->d_ghost[f]; }
-  tp->halo[0] = c->halo[0];
-  tp->halo[1] = c->halo[1];
+  tp->halo[0] = c->comm_kind ? c->d_halo[0] : c->halo[0];  // library-owned planes when a comm is set
+  tp->halo[1] = c->comm_kind ? c->d_halo[1] : c->halo[1];
   if (with_shift)
     for (int a = 0; a < c->grid.dx; ++a) {
       if (half >= 0) shift_delta_half(half, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
@@ -505,6 +571,186 @@ bool valid_N(int N) { return N == 8 || N == 16 || N == 32; }
 
 }  // namespace
 
+// ------------------------------------------------------------------ a2: slab halo exchange
+// NCCL is resolved at run time (the copy torch already loaded, else the system libnccl.so.2), so
+// libfks has no link-time NCCL dependency and builds without a GPU.
+namespace {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) getUniqueId;
+  decltype(&ncclCommInitRank) commInitRank;
+  decltype(&ncclCommDestroy) commDestroy;
+  decltype(&ncclGroupStart) groupStart;
+  decltype(&ncclGroupEnd) groupEnd;
+  decltype(&ncclSend) send;
+  decltype(&ncclRecv) recv;
+};
+
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static int state = 0;  // 0 untried, 1 ok, -1 unavailable
+  if (state == 0) {
+    state = -1;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+      api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+      api.send = (decltype(api.send))dlsym(h, "ncclSend");
+      api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+      if (api.getUniqueId && api.commInitRank && api.commDestroy && api.groupStart && api.groupEnd && api.send &&
+          api.recv)
+        state = 1;
+    }
+  }
+  return state == 1 ? &api : nullptr;
+}
+
+// The velocity slices k_a a step moves across the slab faces: `down` (delta = +1: the lower rank's
+// cells read one plane up, i.e. my first plane) and `up` (delta = -1).  false if |delta| > 1.
+bool halo_plan(int64_t n, int N, double L, double dt, double h, fks::SliceList* down, fks::SliceList* up) {
+  int8_t d[fks::kMaxN];
+  shift_delta(n, N, L, dt, h, d);
+  down->n = up->n = 0;
+  for (int k = 0; k < N; ++k) {
+    if (d[k] < -1 || d[k] > 1) return false;  // halo width 1 (reading #15)
+    if (d[k] > 0) down->k[down->n++] = (int8_t)k;
+    if (d[k] < 0) up->k[up->n++] = (int8_t)k;
+  }
+  return true;
+}
+
+bool comm_active(const fks_ctx* c) { return c->comm_kind != 0 && (c->peer[0] >= 0 || c->peer[1] >= 0); }
+
+// Neighbours, plane size and buffers for the slab axis a = dx - 1 (each rank keeps all
+// velocities of its slab, ghost planes are exchanged every step).
+fks_status comm_setup(fks_ctx* c, int rank, int nranks) {
+  const int a = c->grid.dx - 1;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->pc = 1;
+  for (int b = 0; b < a; ++b) c->pc *= c->grid.M[b];
+  c->peer[0] = c->grid.bc[2 * a] == FKS_BC_HALO ? (rank - 1 + nranks) % nranks : -1;
+  c->peer[1] = c->grid.bc[2 * a + 1] == FKS_BC_HALO ? (rank + 1) % nranks : -1;
+  if (!c->s_comm && cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking) != cudaSuccess) return FKS_E_CUDA;
+  for (cudaEvent_t* e : {&c->ev_ready, &c->ev_halo, &c->ev_packed})
+    if (!*e && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return FKS_E_CUDA;
+  const size_t bytes = (size_t)c->pc * c->n * sizeof(double);
+  for (int f = 0; f < 2; ++f) {
+    if (c->peer[f] < 0) continue;
+    for (double** b : {&c->d_halo[f], &c->d_send[f], &c->d_recv[f]})
+      if (!*b && cudaMalloc(b, bytes) != cudaSuccess) return FKS_E_NOMEM;
+  }
+  c->posted = -1;
+  return update_comm_lists(c);
+}
+
+size_t slice_elems(const fks_ctx* c, const fks::SliceList& sl) {
+  return (size_t)c->pc * sl.n * (c->dv == 3 ? c->N * c->N : c->N);
+}
+
+// Pack and send this step's boundary planes: to the lower neighbour the slices k_a with delta > 0
+// (its cells read one plane up), to the upper one those with delta < 0 -- only the velocities whose
+// FKS shift crosses the face; receive the mirror sets into the halo planes.
+fks_status halo_post_impl(fks_ctx* c, const double* f_in) {
+  if (!comm_active(c) || c->posted == c->step_n) return FKS_OK;
+  const int a = c->grid.dx - 1;
+  fks::SliceList down{}, up{};
+  if (!halo_plan(c->step_n, c->N, c->L, c->dt, c->grid.h, &down, &up)) return FKS_E_UNSUPPORTED;
+  c->send_sl[0] = down;  // my first plane -> lower neighbour's hi halo
+  c->send_sl[1] = up;    // my last plane  -> upper neighbour's lo halo
+  c->recv_sl[0] = up;    // my lo halo <- lower neighbour's last plane
+  c->recv_sl[1] = down;  // my hi halo <- upper neighbour's first plane
+  if (cudaEventRecord(c->ev_ready, c->stream) != cudaSuccess ||
+      cudaStreamWaitEvent(c->s_comm, c->ev_ready, 0) != cudaSuccess)
+    return FKS_E_CUDA;
+  const int64_t first[2] = {0, (c->grid.M[a] - 1) * c->pc};
+  c->bytes_sent = 0;
+  for (int f = 0; f < 2; ++f) {
+    if (c->peer[f] < 0) continue;
+    if (fks::launch_halo_pack(f_in, first[f], (int)c->pc, c->n, c->N, c->dv, a, c->send_sl[f], c->d_send[f], false,
+                              c->s_comm) != cudaSuccess)
+      return FKS_E_CUDA;
+    c->launches++;
+    c->bytes_sent += (int64_t)slice_elems(c, c->send_sl[f]) * 8;
+  }
+  if (c->comm_kind == 1) {
+    const NcclApi* nc = nccl_api();
+    if (!nc) return FKS_E_NCCL;
+    // fixed issue order (data moving up before data moving down, sends before receives): with two
+    // ranks on a periodic axis both neighbours are the same peer and NCCL matches in issue order
+    bool ok = nc->groupStart() == ncclSuccess;
+    if (c->peer[1] >= 0 && ok)
+      ok = nc->send(c->d_send[1], slice_elems(c, c->send_sl[1]), ncclFloat64, c->peer[1], c->nccl, c->s_comm) == ncclSuccess;
+    if (c->peer[0] >= 0 && ok)
+      ok = nc->send(c->d_send[0], slice_elems(c, c->send_sl[0]), ncclFloat64, c->peer[0], c->nccl, c->s_comm) == ncclSuccess;
+    if (c->peer[0] >= 0 && ok)
+      ok = nc->recv(c->d_recv[0], slice_elems(c, c->recv_sl[0]), ncclFloat64, c->peer[0], c->nccl, c->s_comm) == ncclSuccess;
+    if (c->peer[1] >= 0 && ok)
+      ok = nc->recv(c->d_recv[1], slice_elems(c, c->recv_sl[1]), ncclFloat64, c->peer[1], c->nccl, c->s_comm) == ncclSuccess;
+    if (nc->groupEnd() != ncclSuccess || !ok) return FKS_E_NCCL;
+    for (int f = 0; f < 2; ++f) {
+      if (c->peer[f] < 0) continue;
+      if (fks::launch_halo_pack(c->d_halo[f], 0, (int)c->pc, c->n, c->N, c->dv, a, c->recv_sl[f], c->d_recv[f], true,
+                                c->s_comm) != cudaSuccess)
+        return FKS_E_CUDA;
+      c->launches++;
+    }
+    if (cudaEventRecord(c->ev_halo, c->s_comm) != cudaSuccess) return FKS_E_CUDA;
+  } else if (cudaEventRecord(c->ev_packed, c->s_comm) != cudaSuccess) {
+    return FKS_E_CUDA;
+  }
+  c->posted = c->step_n;
+  return FKS_OK;
+}
+
+// Make the halo planes of this step visible to the context stream.  Loopback: pull the neighbours'
+// packed planes (they must have posted this step) with device copies, unpack, and finish before
+// returning so a neighbour's next post cannot overwrite its send buffer under the copy.
+fks_status halo_wait_impl(fks_ctx* c) {
+  if (!comm_active(c)) return FKS_OK;
+  if (c->posted != c->step_n) return FKS_E_STATE;
+  if (c->comm_kind == 2) {
+    const int a = c->grid.dx - 1;
+    for (int f = 0; f < 2; ++f) {
+      if (c->peer[f] < 0) continue;
+      fks_ctx* q = c->loop->ctx[c->peer[f]];
+      if (!q || q->posted != c->step_n) return FKS_E_STATE;
+      if (cudaStreamWaitEvent(c->s_comm, q->ev_packed, 0) != cudaSuccess ||
+          cudaMemcpyAsync(c->d_recv[f], q->d_send[1 - f], slice_elems(c, c->recv_sl[f]) * sizeof(double),
+                          cudaMemcpyDeviceToDevice, c->s_comm) != cudaSuccess)
+        return FKS_E_CUDA;
+      if (fks::launch_halo_pack(c->d_halo[f], 0, (int)c->pc, c->n, c->N, c->dv, a, c->recv_sl[f], c->d_recv[f], true,
+                                c->s_comm) != cudaSuccess)
+        return FKS_E_CUDA;
+      c->launches++;
+    }
+    if (cudaEventRecord(c->ev_halo, c->s_comm) != cudaSuccess || cudaStreamSynchronize(c->s_comm) != cudaSuccess)
+      return FKS_E_CUDA;
+  }
+  return cuda_fail(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+}
+
+// Loopback: every neighbour must have posted this step before anything is enqueued here.
+fks_status loop_peers_posted(const fks_ctx* c) {
+  if (c->comm_kind != 2) return FKS_OK;
+  for (int f = 0; f < 2; ++f) {
+    if (c->peer[f] < 0) continue;
+    const fks_ctx* q = c->loop->ctx[c->peer[f]];
+    if (!q || q->posted != c->step_n) return FKS_E_STATE;
+  }
+  return FKS_OK;
+}
+
+fks_status halo_sync(fks_ctx* c, const double* f_in) {
+  fks_status st = halo_post_impl(c, f_in);
+  if (st == FKS_OK) st = loop_peers_posted(c);
+  return st != FKS_OK ? st : halo_wait_impl(c);
+}
+}  // namespace
+
 extern "C" {
 
 const char* fks_strerror(fks_status s) {
@@ -538,6 +784,19 @@ fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, doubl
   if (w_host) std::memcpy(w_host, d.w.data(), d.w.size() * sizeof(double));
   if (e_host) std::memcpy(e_host, d.e.data(), d.e.size() * sizeof(double));
   if (scale) *scale = node_scale(dv, L, kernel_const, kernel_gamma);
+  return FKS_OK;
+}
+
+fks_status fks_host_halo_slices(int64_t n, int Nv, double L, double dt, double h, int8_t* to_lower, int* n_lower,
+                                int8_t* to_upper, int* n_upper) {
+  if (Nv <= 0 || Nv > fks::kMaxN || !(L > 0) || !(h > 0) || n < 0 || !to_lower || !to_upper || !n_lower || !n_upper)
+    return FKS_E_INVAL;
+  fks::SliceList down{}, up{};
+  if (!halo_plan(n, Nv, L, dt, h, &down, &up)) return FKS_E_UNSUPPORTED;
+  for (int i = 0; i < down.n; ++i) to_lower[i] = down.k[i];
+  for (int i = 0; i < up.n; ++i) to_upper[i] = up.k[i];
+  *n_lower = down.n;
+  *n_upper = up.n;
   return FKS_OK;
 }
 
@@ -678,6 +937,72 @@ fks_status fks_set_scheme(fks_ctx* c, int splitting, int integrator) {
   return FKS_OK;
 }
 
+fks_status fks_comm_unique_id(void* id_out) {
+  if (!id_out) return FKS_E_INVAL;
+  const NcclApi* nc = nccl_api();
+  if (!nc) return FKS_E_NCCL;
+  ncclUniqueId id;
+  if (nc->getUniqueId(&id) != ncclSuccess) return FKS_E_NCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return FKS_OK;
+}
+
+fks_status fks_set_comm(fks_ctx* c, const void* nccl_unique_id, int rank, int nranks) {
+  if (!c || !nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks || c->grid.dx < 1 || c->comm_kind)
+    return FKS_E_INVAL;
+  if (c->reflect) return FKS_E_UNSUPPORTED;
+  const NcclApi* nc = nccl_api();
+  if (!nc) return FKS_E_NCCL;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  if (nc->commInitRank(&c->nccl, nranks, id, rank) != ncclSuccess) return FKS_E_NCCL;
+  c->comm_kind = 1;
+  return comm_setup(c, rank, nranks);
+}
+
+fks_status fks_comm_loopback_create(int nranks, fks_loopback** out) {
+  if (!out || nranks < 1) return FKS_E_INVAL;
+  fks_loopback* l = new (std::nothrow) fks_loopback();
+  if (!l) return FKS_E_NOMEM;
+  l->nranks = nranks;
+  l->ctx.assign(nranks, nullptr);
+  *out = l;
+  return FKS_OK;
+}
+
+fks_status fks_comm_loopback_destroy(fks_loopback* l) {
+  if (!l) return FKS_E_INVAL;
+  for (fks_ctx* c : l->ctx)
+    if (c) c->loop = nullptr, c->comm_kind = 0;
+  delete l;
+  return FKS_OK;
+}
+
+fks_status fks_set_comm_loopback(fks_ctx* c, fks_loopback* l, int rank) {
+  if (!c || !l || rank < 0 || rank >= l->nranks || l->ctx[rank] || c->grid.dx < 1 || c->comm_kind)
+    return FKS_E_INVAL;
+  if (c->reflect) return FKS_E_UNSUPPORTED;
+  c->comm_kind = 2;
+  c->loop = l;
+  l->ctx[rank] = c;
+  return comm_setup(c, rank, l->nranks);
+}
+
+fks_status fks_halo_post(fks_ctx* c, const double* f_in) {
+  if (!c || !f_in) return FKS_E_INVAL;
+  if (!comm_active(c)) return FKS_OK;
+  if (!(c->dt > 0)) return FKS_E_STATE;  // dt is fixed by the first step / fks_set_state
+  return halo_post_impl(c, f_in);
+}
+
+fks_status fks_get_comm_stats(const fks_ctx* c, int64_t* bytes_sent_last, int* interior_cells, int* boundary_cells) {
+  if (!c) return FKS_E_INVAL;
+  if (bytes_sent_last) *bytes_sent_last = c->bytes_sent;
+  if (interior_cells) *interior_cells = c->ninterior;
+  if (boundary_cells) *boundary_cells = c->nboundary;
+  return FKS_OK;
+}
+
 fks_status fks_set_stream(fks_ctx* c, void* s) {
   if (!c) return FKS_E_INVAL;
   c->stream = (cudaStream_t)s;
@@ -702,7 +1027,7 @@ static fks_status check_dt(fks_ctx* c, double dt) {
       if (c->grid.bc[f] == FKS_BC_HALO) return FKS_E_UNSUPPORTED;
   for (int f = 0; f < 2 * c->grid.dx; ++f) {
     if (c->grid.bc[f] == FKS_BC_GHOST && !c->d_ghost[f]) return FKS_E_STATE;
-    if (c->grid.bc[f] == FKS_BC_HALO && !c->halo[f & 1]) return FKS_E_STATE;
+    if (c->grid.bc[f] == FKS_BC_HALO && !(c->comm_kind ? c->d_halo[f & 1] : c->halo[f & 1])) return FKS_E_STATE;
   }
   if (c->dt == 0.0) c->dt = dt;
   else if (c->dt != dt) return FKS_E_STATE;
@@ -716,12 +1041,14 @@ fks_status fks_transport(fks_ctx* c, const double* f_in, double* f_out, double d
   fks::TransportParams tp;
   st = fill_transport(c, &tp, true);
   if (st != FKS_OK) return st;
+  if ((st = halo_sync(c, f_in)) != FKS_OK) return st;
   cudaError_t e = fks::launch_transport(f_in, f_out, tp, c->d_solid, c->ncells, c->n, c->N, c->dv, c->stream);
   c->launches++;
   if (e != cudaSuccess) return FKS_E_CUDA;
   c->step_n++;
   return FKS_OK;
 }
+
 
 static fks_status ensure_tmp(fks_ctx* c) {
   if (c->d_tmp) return FKS_OK;
@@ -767,6 +1094,7 @@ static fks_status step_scheme(fks_ctx* c, const double* f_in, double* f_out) {
     const double* fstar = f_in;
     if (spatial) {
       if ((st = fill_transport(c, &full, true)) != FKS_OK) return st;
+      if ((st = halo_sync(c, f_in)) != FKS_OK) return st;
       if ((st = transport_pass(c, f_in, tmp, full)) != FKS_OK) return st;
       fstar = tmp;
     }
@@ -802,10 +1130,24 @@ fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   fks::StepParams p = base_params(c, f_in, f_out, 1);
   st = fill_transport(c, &p.tp, true);
   if (st != FKS_OK) return st;
+  if ((st = halo_post_impl(c, f_in)) != FKS_OK) return st;  // a2 on the communication stream
+  if ((st = loop_peers_posted(c)) != FKS_OK) return st;
   if (c->nsolid) {
     if (fks::launch_copy_cells(f_in, f_out, c->d_solid_list, c->nsolid, c->n, c->stream) != cudaSuccess)
       return FKS_E_CUDA;
     c->launches++;
+  }
+  if (comm_active(c)) {
+    // interior cells while the exchange is in flight, then the cells on the HALO-face planes
+    p.cell_list = c->d_interior;
+    p.ncells = c->ninterior;
+    if ((st = run_collision(c, p)) != FKS_OK) return st;
+    if ((st = halo_wait_impl(c)) != FKS_OK) return st;
+    p.cell_list = c->d_boundary;
+    p.ncells = c->nboundary;
+    if ((st = run_collision(c, p)) != FKS_OK) return st;
+    c->step_n++;
+    return FKS_OK;
   }
   p.cell_list = c->nsolid ? c->d_fluid : nullptr;  // identity list: let the kernels prefetch
   p.ncells = c->nfluid;
@@ -847,6 +1189,7 @@ fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt
   p.L = c->L;
   p.dv = 2.0 * c->L / c->N;
   std::memcpy(p.Ginv, c->Ginv, sizeof(p.Ginv));
+  if ((st = halo_sync(c, f_in)) != FKS_OK) return st;
   cudaError_t e = fks::launch_bgk(c->N, c->dv, p, c->sm_count, c->stream);
   c->launches++;
   if (e != cudaSuccess) return FKS_E_CUDA;
@@ -988,6 +1331,22 @@ fks_status fks_finalize(fks_ctx* c) {
   cudaFree(c->d_host_in);
   cudaFree(c->d_host_out);
   cudaFree(c->d_tmp);
+  if (c->nccl) {
+    if (const NcclApi* nc = nccl_api()) nc->commDestroy(c->nccl);
+  }
+  if (c->loop)
+    for (auto& q : c->loop->ctx)
+      if (q == c) q = nullptr;
+  for (int f = 0; f < 2; ++f) {
+    cudaFree(c->d_halo[f]);
+    cudaFree(c->d_send[f]);
+    cudaFree(c->d_recv[f]);
+  }
+  cudaFree(c->d_interior);
+  cudaFree(c->d_boundary);
+  for (cudaEvent_t e : {c->ev_ready, c->ev_halo, c->ev_packed})
+    if (e) cudaEventDestroy(e);
+  if (c->s_comm) cudaStreamDestroy(c->s_comm);
   delete c;
   return FKS_OK;
 }

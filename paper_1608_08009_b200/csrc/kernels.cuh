@@ -24,6 +24,15 @@ int cells_per_block2d(int N);
 cudaError_t launch_transport(const double* f_in, double* f_out, const TransportParams& tp, const uint8_t* solid,
                              int64_t ncells, int n, int N, int dv, cudaStream_t s);
 
+// a2: velocity slices exchanged with a neighbour slab (k along the slab axis).
+struct SliceList {
+  int n;
+  int8_t k[kMaxN];
+};
+// pack: buf = f[first_cell .. first_cell + pc)[slices]; unpack: f[...][slices] = buf.
+cudaError_t launch_halo_pack(const double* f, int64_t first_cell, int pc, int n, int N, int dv, int axis,
+                             const SliceList& sl, double* buf, bool unpack, cudaStream_t s);
+
 // Copy the listed cells f_out[c] = f_in[c] (solid cells in fks_step).
 cudaError_t launch_copy_cells(const double* f_in, double* f_out, const int* cells, int count, int n, cudaStream_t s);
 

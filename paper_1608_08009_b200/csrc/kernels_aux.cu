@@ -90,6 +90,39 @@ cudaError_t launch_copy_cells(const double* f_in, double* f_out, const int* cell
   return cudaGetLastError();
 }
 
+// a2 (slab exchange): pack (or unpack) the velocity slices k_axis in sl.k of `pc` consecutive
+// cells starting at first_cell: buf[p][s][r] <-> f[(first_cell + p) n + k(sl.k[s], r)], r running over
+// the N^{dv-1} indices of the other velocity components in C order.  HBM-bound copy.
+__global__ void k_halo_pack(double* f, int64_t first_cell, int pc, int n, int N, int dv, int axis, SliceList sl,
+                            double* buf, int unpack) {
+  const int m = dv == 3 ? N * N : N;
+  const int64_t total = (int64_t)pc * sl.n * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % m);
+    const int si = (int)((e / m) % sl.n);
+    const int64_t p = e / ((int64_t)m * sl.n);
+    const int ks = sl.k[si];
+    int k;
+    if (axis == 0) k = ks + N * r;                               // kx fixed: (ky[, kz]) = r
+    else if (axis == 1) k = (r % N) + N * (ks + N * (r / N));     // ky fixed: kx = r % N, kz = r / N
+    else k = r + N * N * ks;                                     // kz fixed: a contiguous N^2 block
+    double* fp = f + (first_cell + p) * n + k;
+    if (unpack) *fp = buf[e];
+    else buf[e] = *fp;
+  }
+}
+
+cudaError_t launch_halo_pack(const double* f, int64_t first_cell, int pc, int n, int N, int dv, int axis,
+                             const SliceList& sl, double* buf, bool unpack, cudaStream_t s) {
+  if (pc == 0 || sl.n == 0) return cudaSuccess;
+  const int m = dv == 3 ? N * N : N;
+  const int64_t total = (int64_t)pc * sl.n * m;
+  const int64_t blocks = (total + 255) / 256;
+  k_halo_pack<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(const_cast<double*>(f), first_cell, pc,
+                                                                               n, N, dv, axis, sl, buf, unpack ? 1 : 0);
+  return cudaGetLastError();
+}
+
 // a10: one CTA per cell (persistent), 16-byte loads, fixed-order reduction (warp
 // shuffles, then warps in order): deterministic.  HBM-bound: 8 B read per phase-space point.
 template <int N, int DV>

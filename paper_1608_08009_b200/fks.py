@@ -92,6 +92,27 @@ class Context:
         """NEXT-4: splitting SPLIT_LIE / SPLIT_STRANG, integrator TIME_EULER / TIME_HEUN (fks_set_scheme)."""
         check(self._lib.fks_set_scheme(self.handle, int(splitting), int(integrator)), "fks_set_scheme")
 
+    # ---- a2: the slab exchange inside the library -----------------------------------------
+    def set_comm(self, unique_id, rank, nranks):
+        """fks_set_comm with a 128-byte NCCL unique id (bytes) from comm_unique_id() on one rank."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        check(self._lib.fks_set_comm(self.handle, buf, int(rank), int(nranks)), "fks_set_comm")
+
+    def set_comm_loopback(self, loop, rank):
+        """fks_set_comm_loopback: join an in-process Loopback group as `rank`."""
+        check(self._lib.fks_set_comm_loopback(self.handle, loop.handle, int(rank)), "fks_set_comm_loopback")
+        self._loop_ref = loop
+
+    def halo_post(self, f_in):
+        check(self._lib.fks_halo_post(self.handle, _ptr(f_in)), "fks_halo_post")
+
+    def comm_stats(self):
+        """(bytes sent by the last exchange, interior fluid cells, boundary fluid cells)."""
+        b, i, o = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int()
+        check(self._lib.fks_get_comm_stats(self.handle, ctypes.byref(b), ctypes.byref(i), ctypes.byref(o)),
+              "fks_get_comm_stats")
+        return b.value, i.value, o.value
+
     def set_stream(self, stream):
         """stream: a torch.cuda.Stream (or None for the default stream)."""
         check(self._lib.fks_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream if stream else 0)),
@@ -135,6 +156,31 @@ class Context:
 
     def launch_count(self):
         return int(self._lib.fks_launch_count(self.handle))
+
+
+class Loopback:
+    """fks_comm_loopback_create: an in-process communicator for `nranks` contexts on one device."""
+
+    def __init__(self, nranks):
+        self._lib = load()
+        h = ctypes.c_void_p()
+        check(self._lib.fks_comm_loopback_create(int(nranks), ctypes.byref(h)), "fks_comm_loopback_create")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.fks_comm_loopback_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
+def comm_unique_id():
+    """fks_comm_unique_id: 128 bytes to broadcast to every rank before fks_set_comm."""
+    buf = ctypes.create_string_buffer(128)
+    check(load().fks_comm_unique_id(buf), "fks_comm_unique_id")
+    return buf.raw
 
 
 # ---- function-style aliases with the C names ---------------------------------------------
@@ -184,3 +230,13 @@ def host_shift(n, Nv, L, dt, h):
     check(load().fks_host_shift(int(n), Nv, float(L), float(dt), float(h),
                                 out.ctypes.data_as(ctypes.POINTER(ctypes.c_int8))), "fks_host_shift")
     return out
+
+
+def host_halo_slices(n, Nv, L, dt, h):
+    """fks_host_halo_slices: (slices sent to the lower rank, slices sent to the upper rank) of step n."""
+    lo, hi = np.zeros(Nv, dtype=np.int8), np.zeros(Nv, dtype=np.int8)
+    nl, nh = ctypes.c_int(), ctypes.c_int()
+    p8 = ctypes.POINTER(ctypes.c_int8)
+    check(load().fks_host_halo_slices(int(n), Nv, float(L), float(dt), float(h), lo.ctypes.data_as(p8), ctypes.byref(nl),
+                                      hi.ctypes.data_as(p8), ctypes.byref(nh)), "fks_host_halo_slices")
+    return lo[:nl.value].astype(np.int64), hi[:nh.value].astype(np.int64)

@@ -141,8 +141,25 @@ class HaloExchange:
         return self.lo, self.hi
 
 
+def init_libfks_comm(ctx, rank, world, group=None, device=None):
+    """a2 inside libfks (fks_set_comm): rank 0 draws the NCCL unique id, torch.distributed broadcasts
+    the 128 bytes, every rank builds the library's own communicator.  Afterwards ctx.step does the
+    exchange itself (only the crossing velocity slices, overlapped with the interior cells)."""
+    import torch
+    import torch.distributed as dist
+    from . import fks
+    dev = device if device is not None else ("cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(fks.comm_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, 0, group=group)
+    ctx.set_comm(bytes(t.cpu().numpy().tobytes()), rank, world)
+
+
 class DistributedStep:
-    """fks_step on one rank's slab with the halo exchange in front (a2 -> a1..a9)."""
+    """fks_step on one rank's slab with a torch.distributed halo exchange of whole planes in front
+    (a2 -> a1..a9).  The production path is init_libfks_comm (the exchange inside the library);
+    this class remains for CPU (gloo) checks of the host logic."""
 
     def __init__(self, ctx, slab, n, device, group=None):
         self.ctx, self.x = ctx, HaloExchange(slab, n, device, group=group)

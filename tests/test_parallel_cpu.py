@@ -106,3 +106,89 @@ def test_halo_exchange_gloo(case, world):
     out = ctx.Manager().dict()
     mp.start_processes(_worker, args=(world, _free_port(), case, out), nprocs=world, start_method="spawn")
     assert dict(out) == {r: True for r in range(world)}
+
+
+def _worker_libplan(rank, world, port, case, out):
+    """a2 as libfks does it (fks_set_comm): per step only the velocity slices the library's plan
+    names (fks_host_halo_slices) are sent, packed [plane cells][slices][other components]; the
+    neighbour planes start as NaN, so a slice the transport needs but the plan omits would show."""
+    from paper_1608_08009_b200 import fks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dx, dv, M, N, L, bc = CASES[case]
+        n = N ** dv
+        F, ghosts = _global_state(case)
+        slab = parallel.decompose(dx, M, bc, world, rank)
+        pc = slab.plane_cells
+        vshape = (N,) * dv
+        ax = dv - 1 - (dx - 1)           # array axis of velocity component dx - 1 (layout [kz, ky, kx])
+        local = parallel.local_slice(slab, F.reshape(-1, *vshape))
+        h, dt = 0.1, 0.09 / (L - L / N)
+        ok = True
+        for step in range(4):
+            down, up = fks.host_halo_slices(step, N, L, dt, h)
+            d = transport.shift_delta(step, N, L, dt, h)
+            ok &= set(down) == set(np.nonzero(d > 0)[0]) and set(up) == set(np.nonzero(d < 0)[0])
+            first, last = local[:pc], local[-pc:]
+            send_lo = np.ascontiguousarray(np.take(first, down, axis=1 + ax))
+            send_hi = np.ascontiguousarray(np.take(last, up, axis=1 + ax))
+            lo_r, hi_r = slab.lower(), slab.upper()
+            rlo = np.empty(send_hi.shape) if lo_r is not None else None   # lower's last plane, `up` slices
+            rhi = np.empty(send_lo.shape) if hi_r is not None else None   # upper's first plane, `down` slices
+            ops = []
+            if hi_r is not None:
+                ops.append(dist.P2POp(dist.isend, torch.from_numpy(send_hi), hi_r, None, 0))
+            if lo_r is not None:
+                ops.append(dist.P2POp(dist.isend, torch.from_numpy(send_lo), lo_r, None, 1))
+            if lo_r is not None:
+                t_lo = torch.from_numpy(rlo)
+                ops.append(dist.P2POp(dist.irecv, t_lo, lo_r, None, 0))
+            if hi_r is not None:
+                t_hi = torch.from_numpy(rhi)
+                ops.append(dist.P2POp(dist.irecv, t_hi, hi_r, None, 1))
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            pieces = []
+            if lo_r is not None:
+                plane = np.full((pc,) + vshape, np.nan)
+                idx = [slice(None)] * (1 + dv)
+                idx[1 + ax] = up
+                plane[tuple(idx)] = t_lo.numpy()
+                pieces.append(plane)
+            pieces.append(local)
+            if hi_r is not None:
+                plane = np.full((pc,) + vshape, np.nan)
+                idx = [slice(None)] * (1 + dv)
+                idx[1 + ax] = down
+                plane[tuple(idx)] = t_hi.numpy()
+                pieces.append(plane)
+            ext = np.concatenate(pieces)
+            Mext = list(M)
+            Mext[dx - 1] = ext.shape[0] // pc
+            ext = ext.reshape(tuple(Mext[::-1]) + vshape)
+            bc_ext = list(bc)
+            if slab.world > 1 and slab.periodic:
+                bc_ext[2 * (dx - 1)] = bc_ext[2 * (dx - 1) + 1] = BC_OUTFLOW
+            ref = transport.gather(F, step, dx, dv, N, L, dt, h, bc, ghosts).reshape(-1, n)
+            got = transport.gather(ext, step, dx, dv, N, L, dt, h, bc_ext, ghosts).reshape(-1, n)
+            off = pc if lo_r is not None else 0
+            mine = got[off:off + local.shape[0]]
+            ok &= bool(np.array_equal(mine, ref[slab.lo * pc:slab.hi * pc]))
+            # bytes on the wire per step = what fks_get_comm_stats reports: pc x slices x N^(dv-1) x 8
+            ok &= send_lo.nbytes == pc * len(down) * N ** (dv - 1) * 8
+        out[rank] = ok
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world", [("2d_space_3d_vel", 2), ("1d_ring", 2), ("3d_space", 3)])
+def test_libfks_halo_plan_gloo(case, world):
+    """The library's exchange plan (only delta != 0 slices cross a face) is sufficient: the oracle's
+    transport on the slab plus the partially filled neighbour planes equals the global transport
+    bitwise, over several steps, for 2-3 ranks on CPU (gloo)."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker_libplan, args=(world, _free_port(), case, out), nprocs=world, start_method="spawn")
+    assert dict(out) == {r: True for r in range(world)}
