@@ -5,11 +5,15 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libfks.so")
-SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels3d.cu", "kernels_aux.cu", "kernels_bgk.cu"]
+# FKS_CHECKS=1: the checked build (bounds checks + traps in every kernel) as
+# libfks_checked.so, objects in csrc/checked/ -- load it with FKS_LIB_VARIANT=checked.
+CHECKED = bool(os.environ.get("FKS_CHECKS"))
+LIB = os.path.join(HERE, "libfks_checked.so" if CHECKED else "libfks.so")
+OBJDIR = os.path.join(CSRC, "checked") if CHECKED else CSRC
+SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels2d64.cu", "kernels3d.cu", "kernels_aux.cu", "kernels_bgk.cu"]
 HEADERS = ["fft.cuh", "common.cuh", "kernels.cuh", os.path.join("..", "..", "include", "fks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + os.environ.get("FKS_NVCC_EXTRA", "").split() + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + (["-DFKS_CHECKS"] if CHECKED else []) + os.environ.get("FKS_NVCC_EXTRA", "").split() + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v",
          "--expt-relaxed-constexpr"]
 
@@ -24,13 +28,14 @@ def _stale():
 
 def _compile(s, verbose):
     src = os.path.join(CSRC, s)
-    obj = os.path.join(CSRC, s.replace(".cu", ".o"))
+    os.makedirs(OBJDIR, exist_ok=True)
+    obj = os.path.join(OBJDIR, s.replace(".cu", ".o"))
     r = subprocess.run([NVCC, *FLAGS, "-c", src, "-o", obj], capture_output=True, text=True)
     if verbose or r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {s}")
-    with open(os.path.join(CSRC, s.replace(".cu", ".ptxas.txt")), "w") as fh:
+    with open(os.path.join(OBJDIR, s.replace(".cu", ".ptxas.txt")), "w") as fh:
         fh.write(r.stderr)
     return obj
 

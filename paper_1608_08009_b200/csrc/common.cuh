@@ -5,7 +5,20 @@
 
 namespace fks {
 
-constexpr int kMaxN = 32;
+#ifndef FKS_KMAXN
+#define FKS_KMAXN 64
+#endif
+constexpr int kMaxN = FKS_KMAXN;  // velocity nodes per axis (N = 64: 2D only)
+
+// Checked build (FKS_CHECKS=1 python -m paper_1608_08009_b200.build -> libfks_checked.so): every
+// global / exchange-ring / table / shared-memory / TMEM index the kernels form is range-checked and
+// the kernel traps on a violation -- the bounds-and-asserts substitute for compute-sanitizer, which
+// this GPU pool does not allow (profiles/r02_sanitizer.txt).  Compiled out otherwise.
+#ifdef FKS_CHECKS
+#define FKS_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define FKS_CHECK(cond) do { } while (0)
+#endif
 
 // a1 + a3: per-step shift table and boundary description.
 struct TransportParams {
@@ -20,6 +33,8 @@ struct TransportParams {
   const double* ghost[6];  // ghost vectors (n values) of GHOST faces, device memory
   const double* halo[2];   // HALO faces of the slowest axis: neighbour rank's boundary plane
                            // [plane cells][n] (cells in C order over the other axes)
+  int64_t ncells_total;    // local cells of the state arrays (checked build)
+  int64_t plane_cells;     // cells per plane of the slowest axis (checked build)
 };
 
 struct StepParams {
@@ -35,6 +50,7 @@ struct StepParams {
   int mode;                  // 0 = collide (write Q), 1 = step (project + Euler),
                              // 2 = Heun stage: f_out = (f_base + f_in + dt/tau Pi Q(f_in)) / 2 (NEXT-4)
   const double* f_base;      // mode 2: f* of the step [cells][n] (same cell indices as f_in)
+  int64_t table_elems;       // double2 entries behind `tables` (checked build)
   int project;               // apply a8
   double dt_tau;             // dt / tau
   double L, dv;              // velocity box half-width and spacing
@@ -113,9 +129,14 @@ __device__ __forceinline__ const double* source_base(const double* __restrict__ 
     }
   }
   if (gface >= 0) {
-    if (tp.bc[gface] == 3) return tp.halo[gface & 1] + hplane * n;
+    if (tp.bc[gface] == 3) {
+      FKS_CHECK(tp.halo[gface & 1] != nullptr && hplane >= 0 && hplane < tp.plane_cells);
+      return tp.halo[gface & 1] + hplane * n;
+    }
+    FKS_CHECK(tp.ghost[gface] != nullptr);
     return tp.ghost[gface];
   }
+  FKS_CHECK(src >= 0 && src < tp.ncells_total);
   return F + src * n;
 }
 
@@ -148,6 +169,7 @@ __device__ __forceinline__ const double* source_resolve(const double* __restrict
           idx += (int64_t)(b == a ? nb : c[b]) * stride;
           stride *= tp.M[b];
         }
+        FKS_CHECK(idx >= 0 && idx < tp.ncells_total);
         is_solid = tp.solid[idx] != 0;
       }
       if (is_solid) {
@@ -172,12 +194,15 @@ __device__ __forceinline__ int mirror_k(int k, int kx, int ky, int kz, int flip,
 __device__ __forceinline__ double gather_fstar(const double* __restrict__ F, const TransportParams& tp,
                                                const CellCoord& cc, int k, int kx, int ky, int kz, int n,
                                                const int8_t (*delta)[kMaxN]) {
+  FKS_CHECK(k >= 0 && k < n && cc.cell >= 0 && cc.cell < tp.ncells_total);
   if (tp.dx == 0) return F[cc.cell * n + k];
   int d[3] = {delta[0][kx], tp.dx > 1 ? delta[1][ky] : 0, tp.dx > 2 ? delta[2][kz] : 0};
   if (tp.reflect) {
     int flip;
     const double* base = source_resolve(F, tp, cc, d, n, flip);
-    return base[mirror_k(k, kx, ky, kz, flip, tp.Nv)];
+    const int km = mirror_k(k, kx, ky, kz, flip, tp.Nv);
+    FKS_CHECK(km >= 0 && km < n);
+    return base[km];
   }
   return source_base(F, tp, cc, d, n)[k];
 }

@@ -327,6 +327,7 @@ struct fks_ctx {
   int nclusters = 0;       // 3D persistent clusters
   double Ginv[25];
   double2* d_tables = nullptr;
+  int64_t table_elems = 0;
   double2* d_scratch = nullptr;
   unsigned* d_sync = nullptr;  // 3D group counters
   int* d_flag = nullptr;
@@ -422,6 +423,7 @@ fks_status upload_tables(fks_ctx* c) {
   if (c->d_tables) cudaFree(c->d_tables);
   c->d_tables = nullptr;
   if (cudaMalloc(&c->d_tables, T.size() * sizeof(double2)) != cudaSuccess) return FKS_E_NOMEM;
+  c->table_elems = (int64_t)T.size();
   return cuda_fail(cudaMemcpy(c->d_tables, T.data(), T.size() * sizeof(double2), cudaMemcpyHostToDevice));
 }
 
@@ -519,6 +521,9 @@ fks_status fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_
   tp->solid = c->d_solid;
   tp->reflect = (c->reflect && c->d_solid && with_shift) ? 1 : 0;
   tp->Nv = c->N;
+  tp->ncells_total = c->ncells;
+  tp->plane_cells = 1;
+  for (int b = 0; b + 1 < c->grid.dx; ++b) tp->plane_cells *= c->grid.M[b];
   tp->cfl1 = 1;
   for (int a = 0; a < 3; ++a)
     for (int k = 0; k < fks::kMaxN; ++k) tp->cfl1 &= tp->delta[a][k] >= -1 && tp->delta[a][k] <= 1;
@@ -537,6 +542,7 @@ fks::StepParams base_params(fks_ctx* c, const double* f_in, double* f_out, int m
   p.f_in = f_in;
   p.f_out = f_out;
   p.tables = c->d_tables;
+  p.table_elems = c->table_elems;
   p.scratch = c->d_scratch;
   p.sync = c->d_sync;
   p.nonfinite = c->d_flag;
@@ -567,7 +573,9 @@ fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
   return cuda_fail(e);
 }
 
-bool valid_N(int N) { return N == 8 || N == 16 || N == 32; }
+// Velocity nodes per axis: 8, 16, 32 in 2D and 3D, 64 in 2D (P:624-625 quotes 16-64 per axis; the
+// 3D 64^3 transform, 4 MiB per complex field, exceeds the 8-SM group design -- DESIGN.md §10).
+bool valid_N(int N, int dv) { return N == 8 || N == 16 || N == 32 || (N == 64 && dv == 2); }
 
 }  // namespace
 
@@ -770,7 +778,7 @@ const char* fks_strerror(fks_status s) {
 fks_status fks_host_tables(int dv, int Nv, double L, int M_dirs, double R, double kernel_const, double kernel_gamma,
                            double* alpha_host, double* alphap_host, double* D_host, double* w_host, double* e_host,
                            double* scale) {
-  if ((dv != 2 && dv != 3) || !valid_N(Nv) || !(L > 0)) return FKS_E_INVAL;
+  if ((dv != 2 && dv != 3) || !valid_N(Nv, dv) || !(L > 0)) return FKS_E_INVAL;
   if (!valid_gamma(kernel_gamma)) return FKS_E_UNSUPPORTED;
   Dirs d;
   if (!default_dirs(dv, M_dirs, &d)) return FKS_E_UNSUPPORTED;
@@ -810,7 +818,7 @@ fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double k
   if (!grid || !out) return FKS_E_INVAL;
   *out = nullptr;
   const int dv = grid->dv;
-  if ((dv != 2 && dv != 3) || !valid_N(Nv) || !(L > 0) || grid->dx < 0 || grid->dx > 3 || grid->dx > dv)
+  if ((dv != 2 && dv != 3) || !valid_N(Nv, dv) || !(L > 0) || grid->dx < 0 || grid->dx > 3 || grid->dx > dv)
     return FKS_E_INVAL;
   if (!valid_gamma(kernel_gamma)) return FKS_E_UNSUPPORTED;  // NEXT-3: -1 < gamma <= 2 (reading #25)
   int64_t ncells = 1;

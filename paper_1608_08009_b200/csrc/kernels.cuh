@@ -16,6 +16,10 @@ size_t sync_bytes3d();
 // 3D table layout: P CTAs per cell, NP l_y planes per CTA, slabr rows (of N entries) per CTA slab.
 int table_layout3d(int N, int* P, int* NP, int* slabr);
 
+// 2D, N = 64 (kernels2d64.cu: pencils split over lane pairs), 2 cells per CTA.
+cudaError_t launch_step2d64(const StepParams& p, int nblocks, cudaStream_t s);
+int cells_per_block2d64();
+
 // 2D (Maxwell molecules): cells_per_block2d(N) cells per CTA.
 cudaError_t launch_step2d(int N, const StepParams& p, int nblocks, cudaStream_t s);
 int cells_per_block2d(int N);

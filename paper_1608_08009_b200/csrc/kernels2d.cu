@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
   load_delta(p.tp, sdelta);
   if (TAB_SMEM) {
     const int tot = (p.A + 1) * N * HC;
+    FKS_CHECK((int64_t)(p.A + 1) * n <= p.table_elems);
     for (int e = threadIdx.x; e < tot; e += C::THREADS) {
       const int c = e % HC, ly = (e / HC) % N, d = e / (HC * N);
       tab[e] = __ldg(p.tables + (size_t)d * n + ly * N + c);
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
     const bool active = itr < p.ncells;
     const int it = active ? itr : p.ncells - 1;
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    FKS_CHECK(cell >= 0 && cell < p.tp.ncells_total);
     const CellCoord cc = cell_coord(p.tp, cell);
     // the next cell of this group (homogeneous case: a contiguous 8 KB row block) -> L2
     if (p.tp.dx == 0 && tx == 0 && !p.cell_list) {
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(Cfg2<N>::THREADS, 1) k_step2d(const StepParams
                 const int row = neg ? (N - ly) & (N - 1) : ly;
                 tt[i] = tab[((size_t)d * N + row) * HC + tcol];
               } else {
+                FKS_CHECK((int64_t)d * n + ly * N + tx < p.table_elems);
                 tt[i] = __ldg(p.tables + (size_t)d * n + ly * N + tx);
               }
             }
@@ -347,6 +350,7 @@ cudaError_t launch_step2d(int N, const StepParams& p, int nblocks, cudaStream_t 
     case 8: return launch2<8>(p, nblocks, s);
     case 16: return launch2<16>(p, nblocks, s);
     case 32: return launch2<32>(p, nblocks, s);
+    case 64: return launch_step2d64(p, nblocks, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -356,6 +360,7 @@ int cells_per_block2d(int N) {
     case 8: return Cfg2<8>::GROUPS;
     case 16: return Cfg2<16>::GROUPS;
     case 32: return Cfg2<32>::GROUPS;
+    case 64: return cells_per_block2d64();
     default: return 0;
   }
 }

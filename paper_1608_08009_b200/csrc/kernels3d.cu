@@ -348,6 +348,8 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
   const double2* tab_rank = p.tables + (size_t)rank * C::SLAB;  // + direction * P * SLAB
   constexpr size_t TB = C::TBUF_BYTES / 16;  // complex elements per table buffer
   auto load_tab = [&](int j) {  // tg_leader: this group's rows of direction j -> table buffer j & 1
+    FKS_CHECK(j >= 0 && j < D && (int64_t)((size_t)j * P * C::SLAB + (size_t)rank * C::SLAB + (size_t)trow1 * N) <= p.table_elems);
+    FKS_CHECK(trow0 >= 0 && trow1 <= C::SLABR && (size_t)trow1 * N <= TB);
     bulk_load(c.tbuf + (j & 1) * TB + (size_t)trow0 * N, tab_rank + (size_t)j * P * C::SLAB + (size_t)trow0 * N,
               (uint32_t)(trow1 - trow0) * N * 16, c.tbar + (j & 1) * NTG + tgi);
   };
@@ -358,6 +360,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
   unsigned ncell = 0;   // cells done by this group
   for (int it = cid; it < p.ncells; it += c.ncl, ++ncell) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    FKS_CHECK(cell >= 0 && cell < p.tp.ncells_total);
     const CellCoord cc_cell = cell_coord(p.tp, cell);
     const int zpl = rank * NP + tl;  // forward: this thread's j_z plane
     const unsigned par = ncell & 1;
@@ -403,6 +406,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
             const int x = e % N, y = (e / N) % N, zz = rank * NP + e / (N * N);
             const int combo = (c.delta[0][x] + 1) + 3 * (c.delta[1][y] + 1) + 9 * (c.delta[2][zz] + 1);
             const int k = x + N * (y + N * zz);
+            FKS_CHECK(combo >= 0 && combo < 27 && k < n);
             v[j] = c.sbase[combo][c.sflip[combo] ? mirror_k(k, x, y, zz, c.sflip[combo], N) : k];
           }
         } else {
@@ -468,6 +472,7 @@ __device__ __forceinline__ void z_group(const StepParams& p, const Ctx3<N, P>& c
           load_tab(0);
           if (D > 1) load_tab(1);
         }
+        FKS_CHECK(zpl >= 0 && zpl < N && tx < N);
         double2* Wb = c.W + (s_fwd % NB) * C::WBUF + (size_t)zpl * C::WPLANE;
 #pragma unroll
         for (int l = 0; l < N; ++l) Wb[l * N + swz(l, tx)] = cc[l];
@@ -618,6 +623,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
     for (int d = 0; d < D; ++d) {
       TSTAMP(d * 8);
       const int pb = d & 1;
+      FKS_CHECK(tl >= 0 && tl < NP && tx < N && d <= p.A);
       double2* pln = c.pln0 + pb * C::PSLAB;
       mbar_wait(c.wbar + pb * NW + w, (wphase >> pb) & 1u);
       wphase ^= 1u << pb;
@@ -668,6 +674,7 @@ __device__ __forceinline__ void xy_group(const StepParams& p, const Ctx3<N, P>& 
     }
     TSTAMPB(4);
     // a8 + a9: projection and Euler (or write Q)
+    FKS_CHECK(cell >= 0 && cell < p.tp.ncells_total && z < N);
     double* out = p.f_out + cell * (int64_t)n;
     if (p.mode == 0) {
       fs_release();
@@ -790,6 +797,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   c.tl = c.tg / N;
   c.W = p.scratch + (size_t)c.cid * C::NBUF * C::WBUF;
   c.gs = reinterpret_cast<GroupSync*>(p.sync) + c.cid;
+  FKS_CHECK(P <= 16 && C::SMEM <= 232448);
 
   if (t < 32) {  // warp 0 owns the TMEM allocation
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
@@ -811,6 +819,7 @@ __global__ void __launch_bounds__(Cfg3<N, P>::THREADS, 1) k_step3d(const StepPar
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tbase = *tmem_slot;
+  FKS_CHECK((tbase & 0xffffu) + C::TMEM_COLS <= 512u && C::USED_COLS <= C::TMEM_COLS);
   // this thread's TMEM lane: warp quarter base + lane in warp (row field = bits 31..16)
   const uint32_t taddr = tbase + ((uint32_t)(32 * ((t >> 5) & 3)) << 16);
   if (zg) z_group<N, P>(p, c, taddr);

@@ -12,6 +12,7 @@ __global__ void k_transport(const double* __restrict__ f_in, double* __restrict_
   load_delta(tp, sdelta);
   __syncthreads();
   for (int64_t cell = blockIdx.y; cell < ncells; cell += gridDim.y) {
+    FKS_CHECK(cell < tp.ncells_total);
     const bool is_solid = solid != nullptr && solid[cell];
     const CellCoord cc = cell_coord(tp, cell);
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -45,12 +46,27 @@ __global__ void __launch_bounds__(256) k_transport_cfl1(const double* __restrict
     }
     __syncthreads();
     double* out = f_out + cell * n;
-#pragma unroll 8
-    for (int k = threadIdx.x; k < n; k += 256) {
-      const int kx = k % N, ky = (k / N) % N, kz = DV == 3 ? k / (N * N) : 0;
-      const int combo = (sdelta[0][kx] + 1) + 3 * (sdelta[1][ky] + 1) + 9 * (sdelta[2][kz] + 1);
-      const int ks = sflip[combo] ? mirror_k(k, kx, ky, kz, sflip[combo], N) : k;
-      out[k] = __ldg(sbase[combo] + ks);
+    // k = tid + 256 i: kx = tid % N is loop-invariant (N divides 256); all UNR loads of a batch are
+    // issued before its stores (the round-1 loop relied on the compiler for that and lost ~25 % when
+    // an unrelated change shifted its register allocation)
+    constexpr int UNR = n >= 2048 ? 8 : (n >= 256 ? n / 256 : 1);  // n / (256 UNR) whole batches
+    static_assert(n < 256 || n % (256 * UNR) == 0, "whole batches");
+    const int kx = threadIdx.x % N;
+    const int dx0 = sdelta[0][kx] + 1;
+#pragma unroll 1
+    for (int k0 = threadIdx.x; k0 < n; k0 += 256 * UNR) {  // n < 256: threads >= n skip
+      double v[UNR];
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        const int k = k0 + 256 * j;
+        const int ky = (k / N) % N, kz = DV == 3 ? k / (N * N) : 0;
+        const int combo = dx0 + 3 * (sdelta[1][ky] + 1) + 9 * (sdelta[2][kz] + 1);
+        const int ks = sflip[combo] ? mirror_k(k, kx, ky, kz, sflip[combo], N) : k;
+        FKS_CHECK(combo >= 0 && combo < 27 && ks >= 0 && ks < n && cell < tp.ncells_total);
+        v[j] = __ldg(sbase[combo] + ks);
+      }
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) out[k0 + 256 * j] = v[j];
     }
   }
 }
@@ -66,7 +82,7 @@ cudaError_t launch_transport(const double* f_in, double* f_out, const TransportP
   if (cfl1) {
 #define FKS_TR(NN, DD) \
   if (N == NN && dv == DD) { k_transport_cfl1<NN, DD><<<nb, 256, 0, s>>>(f_in, f_out, tp, solid, ncells); return cudaGetLastError(); }
-    FKS_TR(8, 2) FKS_TR(16, 2) FKS_TR(32, 2) FKS_TR(8, 3) FKS_TR(16, 3) FKS_TR(32, 3)
+    FKS_TR(8, 2) FKS_TR(16, 2) FKS_TR(32, 2) FKS_TR(64, 2) FKS_TR(8, 3) FKS_TR(16, 3) FKS_TR(32, 3)
 #undef FKS_TR
   }
   const int threads = 256;
@@ -102,6 +118,7 @@ __global__ void k_halo_pack(double* f, int64_t first_cell, int pc, int n, int N,
     const int si = (int)((e / m) % sl.n);
     const int64_t p = e / ((int64_t)m * sl.n);
     const int ks = sl.k[si];
+    FKS_CHECK(si < sl.n && ks >= 0 && ks < N);
     int k;
     if (axis == 0) k = ks + N * r;                               // kx fixed: (ky[, kz]) = r
     else if (axis == 1) k = (r % N) + N * (ks + N * (r / N));     // ky fixed: kx = r % N, kz = r / N
@@ -226,6 +243,7 @@ cudaError_t launch_moments(const double* f, double* rho, double* u, double* T, i
     if (N == 8) { k_moments_warp<8><<<nw, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
     if (N == 16) { k_moments_warp<16><<<nw, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
     if (N == 32) { k_moments_warp<32><<<nw, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
+    if (N == 64) { k_moments_warp<64><<<nw, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
   }
 #define FKS_MO(NN, DD) \
   if (N == NN && dv == DD) { k_moments<NN, DD><<<nb, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(NT, MINB) k_bgk(const BgkParams p, const int p
   for (int a = 0; a < DV; ++a) vol *= h;
   for (int it = blockIdx.x; it < p.ncells; it += gridDim.x) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    FKS_CHECK(cell >= 0 && cell < p.tp.ncells_total);
     const CellCoord cc = cell_coord(p.tp, cell);
     __syncthreads();  // sdelta loaded / previous cell's sources no longer read
     if (p.tp.dx > 0 && p.tp.cfl1 && threadIdx.x < 27) {
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(256, MINB) k_bgk2w(const BgkParams p) {
   const double h = p.dv, vol = h * h;
   for (int it = blockIdx.x * 8 + wv; it < p.ncells; it += gridDim.x * 8) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
+    FKS_CHECK(cell >= 0 && cell < p.tp.ncells_total);
     const double2* src = reinterpret_cast<const double2*>(p.f_in + cell * n);
     double m[5] = {0, 0, 0, 0, 0};
 #pragma unroll 4
@@ -326,7 +328,7 @@ cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStre
     else k_bgk<NN, DD, 256, 1><<<nb, 256, 0, s>>>(p, pf);                                    \
     return cudaGetLastError();                                                               \
   }
-  FKS_BGK(8, 2) FKS_BGK(16, 2) FKS_BGK(32, 2) FKS_BGK(8, 3) FKS_BGK(16, 3) FKS_BGK(32, 3)
+  FKS_BGK(8, 2) FKS_BGK(16, 2) FKS_BGK(32, 2) FKS_BGK(64, 2) FKS_BGK(8, 3) FKS_BGK(16, 3) FKS_BGK(32, 3)
 #undef FKS_BGK
   return cudaErrorInvalidValue;
 }

@@ -261,3 +261,81 @@ def test_full_size_C3_strang_heun_sampled(torch, fks):
     ref = transport.gather(mid, 0, dxd, dv, N, L, dt, hx, c["bc"], ghosts, cells=sample, delta=d2)
     for i, j in enumerate(sample):
         assert np.max(np.abs(got[j] - ref[i])) <= TOL * np.max(np.abs(ref[i])), j
+
+
+# ---------------------------------------------------------------- N = 64 velocity grids (2D)
+@pytest.mark.parametrize("kind", ["bkw", "random"])
+def test_collide_2d_n64(torch, fks, kind):
+    """2D 64^2, pencils split over lane pairs: Q vs the literal double sum (3 cells)
+    and vs the FFT evaluator (all 9 cells; ragged against the 2 cells per CTA)."""
+    N, L, nc = 64, 12.0, 9
+    f = workloads.family(kind, 2, N, L, nc, seed=71)
+    ctx = fks.Context(2, 0, [nc], N, L, 8)
+    Q = torch.empty(nc, N, N, dtype=torch.float64, device="cuda")
+    ctx.collide(dev(torch, f), Q)
+    ctx.check()
+    tab = tables.build_tables(2, N, L, A=8)
+    Qg = host(Q)
+    assert rel_err_Q(Qg[:2], f[:2], tab, direct=True) <= TOL
+    assert rel_err_Q(Qg, f, tab, direct=False) <= TOL
+
+
+@pytest.mark.parametrize("integ", ["euler", "heun"])
+def test_step_2d_n64_with_transport(torch, fks, integ):
+    """Fused steps on a 1D x 2D grid at N = 64 (ghost / outflow faces, a solid cell), both
+    integrators, three steps against the oracle."""
+    dxd, dv, M, N, L = 1, 2, [7], 64, 12.0
+    bc = [transport.GHOST, transport.OUTFLOW]
+    F, h, dt, ghosts = _spatial(dxd, dv, M, N, L, bc, seed=8)
+    solid = np.zeros((7,), dtype=bool)
+    solid[3] = True
+    ctx = fks.Context(dv, dxd, M, N, L, 8, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_solid(solid)
+    ctx.set_params(tau=0.4)
+    if integ == "heun":
+        ctx.set_scheme(fks.SPLIT_LIE, fks.TIME_HEUN)
+    tab = tables.build_tables(2, N, L, A=8)
+    cfg = dict(dx_dim=dxd, dv=dv, N=N, L=L, dt=dt, dx=h, tau=0.4, bc=bc, ghosts=ghosts, solid=solid)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(3):
+        ctx.step(a, b, dt)
+        a, b = b, a
+        ref = ostep.step(ref, s, cfg, tab, integrator=integ)
+    ctx.check()
+    got = host(a)
+    for i in range(7):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i])), i
+
+
+def test_n64_transport_moments_bgk(torch, fks):
+    """The HBM-bound companions at N = 64: transport bitwise, moments to 1e-13, BGK step to 1e-11."""
+    from oracle import moments as omom
+    dxd, dv, M, N, L = 2, 2, [4, 3], 64, 12.0
+    bc = [transport.PERIODIC, transport.PERIODIC, transport.GHOST, transport.OUTFLOW]
+    F, h, dt, ghosts = _spatial(dxd, dv, M, N, L, bc, seed=9)
+    ctx = fks.Context(dv, dxd, M, N, L, 8, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ctx.transport(a, b, dt)
+    np.testing.assert_array_equal(host(b), transport.gather(F, 0, dxd, dv, N, L, dt, h, bc, ghosts))
+    nc = 12
+    rho = torch.empty(nc, dtype=torch.float64, device="cuda")
+    u = torch.empty(nc, 2, dtype=torch.float64, device="cuda")
+    T = torch.empty(nc, dtype=torch.float64, device="cuda")
+    ctx.moments(a, rho, u, T)
+    ro, uo, To = omom.moments_batch(F.reshape(nc, N, N), dv, N, L)
+    np.testing.assert_allclose(host(rho), ro, rtol=1e-13)
+    np.testing.assert_allclose(host(T), To, rtol=1e-12)
+    f0 = workloads.family("random", 2, N, L, 5, seed=3)
+    c0 = fks.Context(2, 0, [5], N, L, 8)
+    c0.set_params(tau=0.8)
+    out = torch.empty_like(dev(torch, f0))
+    c0.step_bgk(dev(torch, f0), out, 0.05, bgk.NU_RHO, 0.0)
+    ref = bgk.homogeneous_bgk_step(f0, 0.05, 0.8, bgk.NU_RHO, 0.0, 2, N, L)
+    got = host(out)
+    for i in range(5):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
