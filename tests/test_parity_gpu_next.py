@@ -339,3 +339,42 @@ def test_n64_transport_moments_bgk(torch, fks):
     got = host(out)
     for i in range(5):
         assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i]))
+
+
+@pytest.mark.parametrize("specular,cfl", [(False, 0.93), (True, 0.93), (False, 1.6)])
+def test_bgk_3d_n32_with_transport(torch, fks, specular, cfl):
+    """NEXT-2 at 32^3 with transport (the TMEM-resident k_bgk_tmem32: f* parked in tensor memory
+    between the moment pass and the update pass): ghost / outflow faces, a solid cell, specular
+    walls, CFL > 1 (general gather), two steps against the oracle."""
+    dxd, dv, M, N, L = 2, 3, [3, 3], 32, 8.0
+    bc = [transport.GHOST, transport.OUTFLOW, transport.OUTFLOW, transport.PERIODIC]
+    F, h, _, ghosts = _spatial(dxd, dv, M, N, L, bc, seed=12)
+    dt = cfl * h / (L - L / N)
+    solid = np.zeros((3, 3), dtype=bool)
+    solid[1, 1] = True
+    ctx = fks.Context(dv, dxd, M, N, L, 24, h=h, bc=bc)
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    ctx.set_solid(solid)
+    if specular:
+        ctx.set_specular(True)
+    ctx.set_params(tau=0.5)
+    a, b = dev(torch, F), torch.empty_like(dev(torch, F))
+    ref = F.copy()
+    for s in range(2):
+        ctx.step_bgk(a, b, dt, bgk.NU_RHO, 0.0)
+        a, b = b, a
+        if specular:
+            fs = transport.gather_specular(ref, s, dxd, dv, N, L, dt, h, bc, ghosts, solid)
+        else:
+            fs = transport.gather(ref, s, dxd, dv, N, L, dt, h, bc, ghosts)
+        nxt = np.empty_like(ref)
+        for j in range(9):
+            idx = np.unravel_index(j, (3, 3))
+            nxt[idx] = ref[idx] if solid[idx] else bgk.bgk_step_cell(fs[idx], dt, 0.5, bgk.NU_RHO, 0.0, dv, N, L)
+        ref = nxt
+    ctx.check()
+    got = host(a).reshape((-1,) + (N,) * dv)
+    ref = ref.reshape((-1,) + (N,) * dv)
+    for i in range(9):
+        assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i])), i
