@@ -7,9 +7,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 # FKS_CHECKS=1: the checked build (bounds checks + traps in every kernel) as
 # libfks_checked.so, objects in csrc/checked/ -- load it with FKS_LIB_VARIANT=checked.
+# FKS_TIMING=1: the per-phase clock64 instrumentation of kernels3d.cu as libfks_timing.so.
 CHECKED = bool(os.environ.get("FKS_CHECKS"))
-LIB = os.path.join(HERE, "libfks_checked.so" if CHECKED else "libfks.so")
-OBJDIR = os.path.join(CSRC, "checked") if CHECKED else CSRC
+TIMING = bool(os.environ.get("FKS_TIMING"))
+_TAG = "checked" if CHECKED else "timing" if TIMING else None
+LIB = os.path.join(HERE, f"libfks_{_TAG}.so" if _TAG else "libfks.so")
+OBJDIR = os.path.join(CSRC, _TAG) if _TAG else CSRC
 SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels2d64.cu", "kernels3d.cu", "kernels_aux.cu", "kernels_bgk.cu"]
 HEADERS = ["fft.cuh", "common.cuh", "kernels.cuh", os.path.join("..", "..", "include", "fks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

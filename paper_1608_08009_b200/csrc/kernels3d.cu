@@ -31,7 +31,10 @@ namespace fks {
 // Development instrumentation: per-phase clock64 stamps of cluster 0 / CTA 0 (FKS_TIMING builds only).
 #ifdef FKS_TIMING
 __device__ long long g_tstamp[4096];
-#define TSTAMP(slot) do { if (cid == 0 && rank == 0 && (tg == 0) && it == 0) g_tstamp[(slot)] = clock64(); } while (0)
+#ifndef FKS_TIMING_ROUND
+#define FKS_TIMING_ROUND 2  // stamp the group's third cell (steady state)
+#endif
+#define TSTAMP(slot) do { if (cid == 0 && rank == 0 && (tg == 0) && it == FKS_TIMING_ROUND * c.ncl) g_tstamp[(slot)] = clock64(); } while (0)
 // cell boundary: the first cell's epilogue and the second cell's forward (slots 1024..)
 #define TSTAMPB(slot) do { if (cid == 0 && rank == 0 && (tg == 0) && (it == 0 || it == c.ncl)) g_tstamp[1024 + (it != 0) * 16 + (slot)] = clock64(); } while (0)
 #else
