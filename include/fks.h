@@ -120,7 +120,8 @@ fks_status fks_set_halo(fks_ctx* ctx, const double* lo_plane, const double* hi_p
  *   time (dlopen libnccl.so.2, reusing an already loaded copy); FKS_E_NCCL if unavailable or an
  *   NCCL call fails.
  * fks_set_comm: build this rank's communicator (collective over the nranks processes).  dx >= 1;
- *   FKS_E_UNSUPPORTED with specular reflection; once per context.
+ *   once per context.  With specular reflection (fks_set_specular) the boundary planes' solid
+ *   flags travel with the planes, so walls that straddle a slab face reflect as in one domain.
  * fks_comm_loopback_create / fks_set_comm_loopback: the same exchange between contexts of ONE
  *   process through device copies (all ranks on one GPU, driven in turn): every rank must call
  *   fks_halo_post for the step before any rank steps (FKS_E_STATE otherwise).
@@ -137,7 +138,7 @@ fks_status fks_halo_post(fks_ctx* ctx, const double* f_in);
 fks_status fks_get_comm_stats(const fks_ctx* ctx, int64_t* bytes_sent_last, int* interior_cells, int* boundary_cells);
 
 /* Solid mask (host, one byte per local cell, copied): solid cells are not collided and keep
- * their values (reading #19; specular reflection is NEXT work). NULL clears it. */
+ * their values (reading #19; fks_set_specular reflects at them instead). NULL clears it. */
 fks_status fks_set_solid(fks_ctx* ctx, const uint8_t* solid_host);
 
 /* NEXT-1: specular reflection at solid cells instead of the frozen solid values of reading #19
@@ -145,7 +146,9 @@ fks_status fks_set_solid(fks_ctx* ctx, const uint8_t* solid_host);
  * fks_transport / fks_step / fks_step_bgk, a particle whose per-axis move would end in a solid
  * cell is reflected there (velocity component mirrored, k_a -> N-1-k_a) -- the inverse of the
  * forward bounce map, so a closed box conserves mass and energy exactly.  on = 0 restores the
- * default.  FKS_E_UNSUPPORTED with HALO faces (a partitioned grid). */
+ * default.  On a partitioned grid (HALO faces) the neighbours' solid flags come with the library
+ * exchange (fks_set_comm / fks_set_comm_loopback); with caller-owned halo planes (fks_set_halo)
+ * the steps return FKS_E_UNSUPPORTED. */
 fks_status fks_set_specular(fks_ctx* ctx, int on);
 
 /* NEXT-4 (reading #26): the time scheme of fks_step.

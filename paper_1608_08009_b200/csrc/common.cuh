@@ -33,6 +33,8 @@ struct TransportParams {
   const double* ghost[6];  // ghost vectors (n values) of GHOST faces, device memory
   const double* halo[2];   // HALO faces of the slowest axis: neighbour rank's boundary plane
                            // [plane cells][n] (cells in C order over the other axes)
+  const uint8_t* halo_solid[2];  // solid flags of the neighbour planes (specular reflection on a
+                                 // partitioned grid; nullptr: none)
   int64_t ncells_total;    // local cells of the state arrays (checked build)
   int64_t plane_cells;     // cells per plane of the slowest axis (checked build)
 };
@@ -158,19 +160,35 @@ __device__ __forceinline__ const double* source_resolve(const double* __restrict
         if (nb < 0) nb += tp.M[a];
       }
       // the candidate origin is a solid cell only if EVERY coordinate is inside the domain (an
-      // axis undone earlier may have left c[b] outside through an OUTFLOW / GHOST / HALO face)
-      bool inside = nb >= 0 && nb < tp.M[a];
-      for (int b = 0; b < tp.dx; ++b)
-        if (b != a) inside &= c[b] >= 0 && c[b] < tp.M[b];
+      // axis undone earlier may have left c[b] outside through an OUTFLOW / GHOST / HALO face) --
+      // or, on a partitioned grid, inside the neighbour plane of a HALO face of the slab axis
+      // (solid flags exchanged with the planes, tp.halo_solid)
+      const int sa = tp.dx - 1;
+      int hs = -1;  // HALO face whose neighbour plane holds the candidate
+      bool inside = true;
+      int64_t idx = 0, stride = 1;
+      for (int b = 0; b < tp.dx; ++b) {
+        const int cb = b == a ? nb : c[b];
+        if (cb < 0 || cb >= tp.M[b]) {
+          const int face = cb < 0 ? 2 * b : 2 * b + 1;
+          if (b == sa && tp.bc[face] == 3 && (cb == -1 || cb == tp.M[b]) && tp.halo_solid[face & 1]) hs = face & 1;
+          else inside = false;
+        } else if (b < sa) {
+          idx += (int64_t)cb * stride;
+          stride *= tp.M[b];
+        } else {
+          idx += (int64_t)cb * stride;
+        }
+      }
       bool is_solid = false;
       if (inside) {
-        int64_t idx = 0, stride = 1;
-        for (int b = 0; b < tp.dx; ++b) {
-          idx += (int64_t)(b == a ? nb : c[b]) * stride;
-          stride *= tp.M[b];
+        if (hs >= 0) {
+          FKS_CHECK(idx >= 0 && idx < tp.plane_cells);
+          is_solid = tp.halo_solid[hs][idx] != 0;
+        } else {
+          FKS_CHECK(idx >= 0 && idx < tp.ncells_total);
+          is_solid = tp.solid[idx] != 0;
         }
-        FKS_CHECK(idx >= 0 && idx < tp.ncells_total);
-        is_solid = tp.solid[idx] != 0;
       }
       if (is_solid) {
         flip |= 1 << a;

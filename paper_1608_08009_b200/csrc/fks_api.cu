@@ -370,6 +370,8 @@ struct fks_ctx {
   int* d_boundary = nullptr;       // fluid cells on a HALO-face plane
   int nboundary = 0;
   std::vector<uint8_t> h_solid;    // host copy of the solid mask (empty: none)
+  uint8_t* d_halo_solid[2] = {nullptr, nullptr};  // neighbour planes' solid flags (specular + comm)
+  uint8_t* d_zero_mask = nullptr;  // all-fluid mask / plane for contexts without solids (specular)
 };
 
 // Loopback communicator: contexts of one process (one device) exchange through device copies,
@@ -518,8 +520,11 @@ fks_status fill_transport(const fks_ctx* c, fks::TransportParams* tp, bool with_
       if (half >= 0) shift_delta_half(half, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
       else shift_delta(c->step_n, c->N, c->L, c->dt, c->grid.h, tp->delta[a]);
     }
-  tp->solid = c->d_solid;
-  tp->reflect = (c->reflect && c->d_solid && with_shift) ? 1 : 0;
+  tp->solid = c->d_solid ? c->d_solid : c->d_zero_mask;
+  // specular reflection needs solid cells somewhere: local ones, or (partitioned) the neighbours'
+  tp->reflect = (c->reflect && with_shift && (c->d_solid || (c->comm_kind && c->d_zero_mask))) ? 1 : 0;
+  tp->halo_solid[0] = c->comm_kind && c->reflect ? c->d_halo_solid[0] : nullptr;
+  tp->halo_solid[1] = c->comm_kind && c->reflect ? c->d_halo_solid[1] : nullptr;
   tp->Nv = c->N;
   tp->ncells_total = c->ncells;
   tp->plane_cells = 1;
@@ -650,6 +655,14 @@ fks_status comm_setup(fks_ctx* c, int rank, int nranks) {
     if (c->peer[f] < 0) continue;
     for (double** b : {&c->d_halo[f], &c->d_send[f], &c->d_recv[f]})
       if (!*b && cudaMalloc(b, bytes) != cudaSuccess) return FKS_E_NOMEM;
+    if (!c->d_halo_solid[f]) {
+      if (cudaMalloc(&c->d_halo_solid[f], (size_t)c->pc) != cudaSuccess) return FKS_E_NOMEM;
+      cudaMemset(c->d_halo_solid[f], 0, (size_t)c->pc);
+    }
+  }
+  if (!c->d_zero_mask) {  // a local all-fluid mask (also a zero plane to send) for contexts without solids
+    if (cudaMalloc(&c->d_zero_mask, (size_t)c->ncells) != cudaSuccess) return FKS_E_NOMEM;
+    cudaMemset(c->d_zero_mask, 0, (size_t)c->ncells);
   }
   c->posted = -1;
   return update_comm_lists(c);
@@ -698,6 +711,17 @@ fks_status halo_post_impl(fks_ctx* c, const double* f_in) {
       ok = nc->recv(c->d_recv[0], slice_elems(c, c->recv_sl[0]), ncclFloat64, c->peer[0], c->nccl, c->s_comm) == ncclSuccess;
     if (c->peer[1] >= 0 && ok)
       ok = nc->recv(c->d_recv[1], slice_elems(c, c->recv_sl[1]), ncclFloat64, c->peer[1], c->nccl, c->s_comm) == ncclSuccess;
+    if (c->reflect) {  // specular walls: the boundary planes' solid flags travel with the planes
+      const uint8_t* mask = c->d_solid ? c->d_solid : c->d_zero_mask;
+      if (c->peer[1] >= 0 && ok)
+        ok = nc->send(mask + first[1], (size_t)c->pc, ncclUint8, c->peer[1], c->nccl, c->s_comm) == ncclSuccess;
+      if (c->peer[0] >= 0 && ok)
+        ok = nc->send(mask + first[0], (size_t)c->pc, ncclUint8, c->peer[0], c->nccl, c->s_comm) == ncclSuccess;
+      if (c->peer[0] >= 0 && ok)
+        ok = nc->recv(c->d_halo_solid[0], (size_t)c->pc, ncclUint8, c->peer[0], c->nccl, c->s_comm) == ncclSuccess;
+      if (c->peer[1] >= 0 && ok)
+        ok = nc->recv(c->d_halo_solid[1], (size_t)c->pc, ncclUint8, c->peer[1], c->nccl, c->s_comm) == ncclSuccess;
+    }
     if (nc->groupEnd() != ncclSuccess || !ok) return FKS_E_NCCL;
     for (int f = 0; f < 2; ++f) {
       if (c->peer[f] < 0) continue;
@@ -734,6 +758,14 @@ fks_status halo_wait_impl(fks_ctx* c) {
                                 c->s_comm) != cudaSuccess)
         return FKS_E_CUDA;
       c->launches++;
+      if (c->reflect) {  // the neighbour's boundary-plane solid flags (lo halo <- its last plane)
+        const int64_t qfirst = f == 0 ? (q->grid.M[a] - 1) * q->pc : 0;
+        const uint8_t* qmask = q->d_solid ? q->d_solid : q->d_zero_mask;
+        cudaError_t e = qmask ? cudaMemcpyAsync(c->d_halo_solid[f], qmask + qfirst, (size_t)c->pc,
+                                                cudaMemcpyDeviceToDevice, c->s_comm)
+                              : cudaMemsetAsync(c->d_halo_solid[f], 0, (size_t)c->pc, c->s_comm);
+        if (e != cudaSuccess) return FKS_E_CUDA;
+      }
     }
     if (cudaEventRecord(c->ev_halo, c->s_comm) != cudaSuccess || cudaStreamSynchronize(c->s_comm) != cudaSuccess)
       return FKS_E_CUDA;
@@ -921,10 +953,7 @@ fks_status fks_set_halo(fks_ctx* c, const double* lo_plane, const double* hi_pla
 
 fks_status fks_set_specular(fks_ctx* c, int on) {
   if (!c) return FKS_E_INVAL;
-  if (on)
-    for (int f = 0; f < 2 * c->grid.dx; ++f)
-      if (c->grid.bc[f] == FKS_BC_HALO) return FKS_E_UNSUPPORTED;
-  c->reflect = on ? 1 : 0;
+  c->reflect = on ? 1 : 0;  // on a partitioned grid the library comm carries the neighbours' solid flags
   return FKS_OK;
 }
 
@@ -958,7 +987,6 @@ fks_status fks_comm_unique_id(void* id_out) {
 fks_status fks_set_comm(fks_ctx* c, const void* nccl_unique_id, int rank, int nranks) {
   if (!c || !nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks || c->grid.dx < 1 || c->comm_kind)
     return FKS_E_INVAL;
-  if (c->reflect) return FKS_E_UNSUPPORTED;
   const NcclApi* nc = nccl_api();
   if (!nc) return FKS_E_NCCL;
   ncclUniqueId id;
@@ -989,7 +1017,6 @@ fks_status fks_comm_loopback_destroy(fks_loopback* l) {
 fks_status fks_set_comm_loopback(fks_ctx* c, fks_loopback* l, int rank) {
   if (!c || !l || rank < 0 || rank >= l->nranks || l->ctx[rank] || c->grid.dx < 1 || c->comm_kind)
     return FKS_E_INVAL;
-  if (c->reflect) return FKS_E_UNSUPPORTED;
   c->comm_kind = 2;
   c->loop = l;
   l->ctx[rank] = c;
@@ -1028,9 +1055,9 @@ fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
 
 static fks_status check_dt(fks_ctx* c, double dt) {
   if (!(dt > 0)) return FKS_E_INVAL;
-  if (c->reflect || (c->split == FKS_SPLIT_STRANG && c->grid.dx > 0))
-    // the neighbour rank's solid cells are not known here; Strang's second half transport would
-    // need a second exchange of the collided state
+  if ((c->reflect && !c->comm_kind) || (c->split == FKS_SPLIT_STRANG && c->grid.dx > 0))
+    // caller-owned halo planes (fks_set_halo) carry no solid flags; Strang's second half transport
+    // would need a second exchange of the collided state
     for (int f = 0; f < 2 * c->grid.dx; ++f)
       if (c->grid.bc[f] == FKS_BC_HALO) return FKS_E_UNSUPPORTED;
   for (int f = 0; f < 2 * c->grid.dx; ++f) {
@@ -1352,6 +1379,9 @@ fks_status fks_finalize(fks_ctx* c) {
   }
   cudaFree(c->d_interior);
   cudaFree(c->d_boundary);
+  cudaFree(c->d_halo_solid[0]);
+  cudaFree(c->d_halo_solid[1]);
+  cudaFree(c->d_zero_mask);
   for (cudaEvent_t e : {c->ev_ready, c->ev_halo, c->ev_packed})
     if (e) cudaEventDestroy(e);
   if (c->s_comm) cudaStreamDestroy(c->s_comm);

@@ -462,12 +462,18 @@ def test_next_entry_points_argument_errors(torch, fks):
     a = dev(torch, f)
     with pytest.raises(fks.FksError):
         ctx.step_bgk(a, a, 0.01, bgk.NU_RHO, 0.0)  # in place is not allowed
-    # specular reflection is refused on a partitioned grid (HALO faces)
+    # specular reflection on a partitioned grid needs the library exchange (the neighbours' solid
+    # flags): with caller-owned halo planes the step is refused
     ctx2 = fks.Context(3, 1, [4], N, L, 24, h=0.1, bc=[fks.BC_HALO, fks.BC_OUTFLOW])
+    ctx2.set_solid(np.array([0, 1, 0, 0], dtype=bool))
+    ctx2.set_specular(True)
+    f4 = dev(torch, workloads.family("smooth", 3, N, L, 4, seed=6))
+    ctx2.set_halo(f4[:1].contiguous(), None)
     with pytest.raises(fks.FksError) as ei:
-        ctx2.set_specular(True)
+        ctx2.step(f4, torch.empty_like(f4), 0.01)
     assert ei.value.status == -2  # FKS_E_UNSUPPORTED
     ctx2.set_specular(False)
+    ctx2.step(f4, torch.empty_like(f4), 0.01)
 
 
 def test_deterministic_and_host_path(torch, fks):

@@ -28,7 +28,7 @@ def fks():
     return _f
 
 
-def _setup(torch, fks, dxd, dv, M, N, L, bc, world, A, h, ghosts, solid, tau=0.5, scheme=None):
+def _setup(torch, fks, dxd, dv, M, N, L, bc, world, A, h, ghosts, solid, tau=0.5, scheme=None, specular=False):
     from paper_1608_08009_b200 import parallel
     ref = fks.Context(dv, dxd, M, N, L, A, h=h, bc=bc)
     slabs = [parallel.decompose(dxd, M, bc, world, r) for r in range(world)]
@@ -43,6 +43,8 @@ def _setup(torch, fks, dxd, dv, M, N, L, bc, world, A, h, ghosts, solid, tau=0.5
         c.set_params(tau=tau)
         if scheme is not None:
             c.set_scheme(*scheme)
+        if specular:
+            c.set_specular(True)
     if solid is not None:
         ref.set_solid(solid)
     for r, (s, c) in enumerate(zip(slabs, ctxs)):
@@ -146,8 +148,8 @@ def test_loopback_full_size_bitwise(torch, fks, name, world):
 
 
 def test_comm_argument_errors(torch, fks):
-    """fks_set_comm_loopback rejects a taken rank, a second comm and specular walls (include/fks.h);
-    a step whose neighbour has not posted is FKS_E_STATE."""
+    """fks_set_comm_loopback rejects a taken rank, a second comm and a rank out of range
+    (include/fks.h); a step whose neighbour has not posted is FKS_E_STATE."""
     N, L, h = 8, 6.0, 0.1
     loop = fks.Loopback(2)
     a = fks.Context(3, 1, [4], N, L, 24, h=h, bc=[fks.BC_GHOST, fks.BC_HALO])
@@ -169,8 +171,45 @@ def test_comm_argument_errors(torch, fks):
         a.step(f, torch.empty_like(f), dt)      # b has not posted step 0
     assert ei.value.status == -7
     c = fks.Context(3, 1, [4], N, L, 24, h=h, bc=[fks.BC_OUTFLOW, fks.BC_OUTFLOW])
-    c.set_solid(np.array([0, 1, 0, 0], dtype=bool))
-    c.set_specular(True)
     with pytest.raises(fks.FksError) as ei:
-        c.set_comm_loopback(fks.Loopback(1), 0)
-    assert ei.value.status == -2
+        c.set_comm_loopback(loop, 3)                # rank out of range
+    assert ei.value.status == -1
+
+
+@pytest.mark.parametrize("dxd,dv,M,N,bc,world,solid_cells", [
+    # solids on both sides of every slab face (the walls straddle the partition)
+    (2, 3, [5, 8], 8, [G_, O, O, O], 2, [(2, 3), (2, 4), (3, 4), (1, 0), (4, 7)]),
+    (2, 2, [6, 9], 16, [P, P, P, P], 3, [(2, 2), (3, 3), (2, 5), (4, 6), (0, 8), (5, 0)]),
+    (3, 3, [4, 3, 6], 8, [O, O, P, P, P, P], 3, [(1, 1, 1), (1, 1, 2), (2, 2, 3), (0, 0, 5), (3, 2, 0)]),
+])
+def test_loopback_specular_bitwise(torch, fks, dxd, dv, M, N, bc, world, solid_cells):
+    """NEXT-1 on a partitioned grid: specular walls that straddle slab faces reflect exactly as in
+    one domain (the boundary planes' solid flags travel with the exchange), transport and fused
+    steps bitwise equal to the single-domain run."""
+    L, h = 6.0, 0.1
+    dt = 0.93 * h / (L - L / N)
+    F, ghosts = _state(dxd, dv, M, N, L, bc, seed=5 + dxd)
+    solid = np.zeros(tuple(M[::-1]), dtype=bool)
+    for cc in solid_cells:
+        solid[tuple(reversed(cc))] = True
+    A = 8 if dv == 2 else 24
+    for call in ("transport", "step"):
+        ref, slabs, ctxs, loop = _setup(torch, fks, dxd, dv, M, N, L, bc, world, A, h, ghosts, solid, specular=True)
+        fn = {"transport": lambda c, a, b: c.transport(a, b, dt), "step": lambda c, a, b: c.step(a, b, dt)}[call]
+        _run(torch, fks, ref, slabs, ctxs, torch.from_numpy(F).cuda(), dt, 3, fn)
+
+
+def test_loopback_specular_C4_full_size(torch, fks):
+    """The C4 geometry at full size with specular walls, 4 slabs of 25 rows: the boxes (rows 42-57)
+    straddle the face between ranks 1 and 2; two fused steps, partitioned == single domain."""
+    c = workloads.config("C4")
+    N, L, A, dv, dxd = c["N"], c["L"], c["A"], c["dv"], c["dx_dim"]
+    M = list(c["cells"][::-1])
+    n = N ** dv
+    nc = int(np.prod(M))
+    v = workloads.initial_state(c, ncells=1).reshape(-1)[:n]
+    s = 1.0 + 0.1 * np.random.default_rng(6).random(nc)
+    G = torch.from_numpy(v[None, :].copy()).cuda() * torch.from_numpy(s[:, None].copy()).cuda()
+    ref, slabs, ctxs, loop = _setup(torch, fks, dxd, dv, M, N, L, c["bc"], 4, A, c["dx"],
+                                    workloads.ghost_vectors(c), workloads.solid_mask(c), tau=c["tau"], specular=True)
+    _run(torch, fks, ref, slabs, ctxs, G, c["dt"], 2, lambda cc, a, b: cc.step(a, b, c["dt"]))
