@@ -442,6 +442,12 @@ def main():
 
     # ---- e2e through the C ABI with host buffers (H2D + step + D2H per step) --------------
     e2e = None
+    state_bytes = ncells * n * 8
+    if not a.no_e2e and F is None and stepper is None and c["dx_dim"] > 0 and state_bytes <= (8 << 30):
+        F = fa.cpu().numpy()  # the spatial configs' state, for the host-buffer path
+    if not a.no_e2e and F is None and c["dx_dim"] > 0:
+        e2e = {"value": None, "unit": "cells/s",
+               "why": f"state of {state_bytes / 2**30:.1f} GiB per copy: pinned host buffers not allocated (limit 8 GiB)"}
     if not a.no_e2e and F is not None and stepper is None:
         hin = torch.from_numpy(np.ascontiguousarray(F)).pin_memory()
         hout = torch.empty_like(hin).pin_memory()

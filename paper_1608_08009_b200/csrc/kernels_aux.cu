@@ -53,8 +53,10 @@ __global__ void __launch_bounds__(256) k_transport_cfl1(const double* __restrict
     static_assert(n < 256 || n % (256 * UNR) == 0, "whole batches");
     const int kx = threadIdx.x % N;
     const int dx0 = sdelta[0][kx] + 1;
+    // few cells (C3: 400 cells for 1184 CTAs): gridDim.y CTAs share a cell, each a range of batches
+    const int kspan = n / (int)gridDim.y;
 #pragma unroll 1
-    for (int k0 = threadIdx.x; k0 < n; k0 += 256 * UNR) {  // n < 256: threads >= n skip
+    for (int k0 = (int)blockIdx.y * kspan + threadIdx.x; k0 < ((int)blockIdx.y + 1) * kspan; k0 += 256 * UNR) {
       double v[UNR];
 #pragma unroll
       for (int j = 0; j < UNR; ++j) {
@@ -80,8 +82,12 @@ cudaError_t launch_transport(const double* f_in, double* f_out, const TransportP
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned nb = (unsigned)(ncells < (int64_t)sms * 8 ? ncells : (int64_t)sms * 8);
   if (cfl1) {
+    // split each cell over gridDim.y CTAs when there are fewer cells than resident CTAs (each part
+    // a whole number of 2048-element batches)
+    int ky = 1;
+    while (n >= 2048 * 2 * ky && (int64_t)nb * ky * 2 <= (int64_t)sms * 8 && ky < 16) ky *= 2;
 #define FKS_TR(NN, DD) \
-  if (N == NN && dv == DD) { k_transport_cfl1<NN, DD><<<nb, 256, 0, s>>>(f_in, f_out, tp, solid, ncells); return cudaGetLastError(); }
+  if (N == NN && dv == DD) { k_transport_cfl1<NN, DD><<<dim3(nb, ky), 256, 0, s>>>(f_in, f_out, tp, solid, ncells); return cudaGetLastError(); }
     FKS_TR(8, 2) FKS_TR(16, 2) FKS_TR(32, 2) FKS_TR(64, 2) FKS_TR(8, 3) FKS_TR(16, 3) FKS_TR(32, 3)
 #undef FKS_TR
   }
