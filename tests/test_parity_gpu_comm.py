@@ -213,3 +213,44 @@ def test_loopback_specular_C4_full_size(torch, fks):
     ref, slabs, ctxs, loop = _setup(torch, fks, dxd, dv, M, N, L, c["bc"], 4, A, c["dx"],
                                     workloads.ghost_vectors(c), workloads.solid_mask(c), tau=c["tau"], specular=True)
     _run(torch, fks, ref, slabs, ctxs, G, c["dt"], 2, lambda cc, a, b: cc.step(a, b, c["dt"]))
+
+
+@pytest.mark.parametrize("dxd,dv,M,N,specular", [(1, 3, [6], 8, False), (2, 2, [4, 5], 16, False),
+                                                 (3, 3, [3, 2, 4], 8, True)])
+def test_nccl_single_rank_ring_bitwise(torch, fks, dxd, dv, M, N, specular):
+    """The real NCCL path on one GPU: a one-rank communicator (fks_comm_unique_id + fks_set_comm,
+    nranks = 1) whose slab axis is a periodic ring of one -- both HALO neighbours are the rank
+    itself, so grouped ncclSend/ncclRecv to self carry the crossing slices (and, with specular walls,
+    the solid flags) -- must reproduce the periodic single-domain run bitwise, three steps."""
+    L, h = 6.0, 0.1
+    dt = 0.93 * h / (L - L / N)
+    bc = [P] * (2 * dxd)
+    F, ghosts = _state(dxd, dv, M, N, L, bc, seed=50 + dxd)
+    A = 8 if dv == 2 else 24
+    ref = fks.Context(dv, dxd, M, N, L, A, h=h, bc=bc)
+    bc_ring = list(bc)
+    bc_ring[2 * (dxd - 1)] = bc_ring[2 * (dxd - 1) + 1] = fks.BC_HALO
+    ring = fks.Context(dv, dxd, M, N, L, A, h=h, bc=bc_ring)
+    if specular:
+        solid = np.zeros(tuple(M[::-1]), dtype=bool)
+        solid.reshape(-1)[[0, 5, len(solid.reshape(-1)) - 1]] = True   # on both slab-face planes
+        for c in (ref, ring):
+            c.set_solid(solid)
+            c.set_specular(True)
+    try:
+        uid = fks.comm_unique_id()
+    except fks.FksError as e:
+        pytest.skip(f"NCCL unavailable: {e}")
+    ring.set_comm(uid, 0, 1)
+    a = torch.from_numpy(F).cuda()
+    ra, rb = a.clone(), torch.empty_like(a)
+    b = torch.empty_like(a)
+    for _ in range(3):
+        ref.step(ra, rb, dt)
+        ring.step(a, b, dt)
+        ring.check()
+        assert torch.equal(b, rb)
+        ra, rb = rb, ra
+        a, b = b, a
+    sent, inner, edge = ring.comm_stats()
+    assert sent > 0 and edge > 0
