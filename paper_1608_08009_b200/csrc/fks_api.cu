@@ -1242,7 +1242,9 @@ static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, doubl
   if (st != FKS_OK) return st;
   const int64_t n = c->n;
   const int64_t per_round = c->dv == 3 ? (int64_t)std::max(1, c->nclusters) : (int64_t)c->sm_count * fks::cells_per_block2d(c->N);
-  int64_t chunk = std::max<int64_t>(per_round * 2, (c->ncells + 11) / 12);
+  int64_t nchunks = 32;  // FKS_HOST_CHUNKS: pipeline depth (C2: 12 chunks 25.6 ms, 32: 24.6 ms; PCIe-bound)
+  if (const char* e = getenv("FKS_HOST_CHUNKS")) nchunks = std::max(1, atoi(e));
+  int64_t chunk = std::max<int64_t>(per_round * 2, (c->ncells + nchunks - 1) / nchunks);
   chunk = (chunk + per_round - 1) / per_round * per_round;  // whole rounds of the persistent grid
   const int nch = (int)((c->ncells + chunk - 1) / chunk);
   if (!c->s_h2d) {

@@ -113,3 +113,48 @@ def test_init_argument_validation(fks):
     with pytest.raises(fks.FksError) as ei:
         fks.Context(3, 0, [4], 8, 7.0, 23)           # no built-in 23-direction set
     assert ei.value.status == -2
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(dv=4), -1),                                   # velocity dimension 2 | 3
+    (dict(dv=2, dx=3), -1),                             # dx <= dv (axis a shifts with velocity component a)
+    (dict(dx=4), -1),
+    (dict(dx=-1), -1),
+    (dict(Nv=24), -1),                                  # not a power of two in {8, 16, 32} (64: 2D)
+    (dict(Nv=4), -1),                                   # N = 4 is out of the supported range
+    (dict(L=0.0), -1),
+    (dict(L=-3.0), -1),
+    (dict(dx=1, M=[0]), -1),                            # empty axis
+    (dict(dx=0, M=[0]), -1),
+    (dict(dx=1, M=[4], h=0.0), -1),                     # spacing
+    (dict(dx=1, M=[4], h=0.1, bc=[5, 0]), -1),          # face kind out of range
+    (dict(dx=2, M=[4, 4], h=0.1, bc=[3, 0, 0, 0]), -1),  # HALO on a non-slab axis
+    (dict(dx=2, M=[70000, 70000], h=0.1), -1),          # more than 2^31 local cells
+    (dict(gamma=-1.0), -2),                             # phi_{R,a} diverges
+    (dict(gamma=2.5), -2),
+    (dict(A=23), -2),                                   # no built-in 23-direction set in 3D
+    (dict(A=0), -2),
+])
+def test_init_rejects_bad_arguments(fks, kw, status):
+    """fks_init validates every argument before touching the device (include/fks.h: argument errors
+    return synchronously with nothing created)."""
+    a = dict(dv=3, dx=0, M=[4], Nv=8, L=7.0, A=24, gamma=None, h=1.0, bc=None)
+    a.update(kw)
+    with pytest.raises(fks.FksError) as ei:
+        fks.Context(a["dv"], a["dx"], a["M"], a["Nv"], a["L"], a["A"], kernel_gamma=a["gamma"], h=a["h"], bc=a["bc"])
+    assert ei.value.status == status
+
+
+def test_host_entry_points_reject_bad_arguments(fks):
+    lib = fks.load()
+    import ctypes
+    out = (ctypes.c_int8 * 64)()
+    n1, n2 = ctypes.c_int(), ctypes.c_int()
+    assert lib.fks_host_shift(0, 0, 1.0, 0.1, 0.1, out) == -1          # Nv
+    assert lib.fks_host_shift(-1, 8, 1.0, 0.1, 0.1, out) == -1         # n < 0
+    assert lib.fks_host_shift(0, 8, 1.0, 0.1, 0.0, out) == -1          # h
+    assert lib.fks_host_halo_slices(0, 8, 5.0, 0.5, 0.1, out, ctypes.byref(n1), out, ctypes.byref(n2)) == -2  # |delta| > 1
+    assert lib.fks_comm_loopback_create(0, ctypes.byref(ctypes.c_void_p())) == -1
+    assert lib.fks_set_scheme(None, 0, 0) == -1
+    assert lib.fks_step(None, None, None, 0.1) == -1
+    assert lib.fks_finalize(None) == -1

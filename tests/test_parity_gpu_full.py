@@ -271,3 +271,45 @@ def test_specular_next_to_outflow_faces(torch, fks, solid_xyz, cfl):
         a, b = b, a
         ref = transport.gather_specular(ref, s, dxd, dv, N, L, dt, h, bc, {}, solid)
     np.testing.assert_array_equal(host(a), ref)
+
+
+def test_configuration_and_state_errors(torch, fks):
+    """The configuration calls and the steps report misuse with the documented status and enqueue
+    nothing (include/fks.h): FKS_E_INVAL for bad arguments, FKS_E_STATE for out-of-order use."""
+    import ctypes
+    N, L, h = 8, 6.0, 0.1
+    bc = [fks.BC_GHOST, fks.BC_OUTFLOW]
+    ctx = fks.Context(3, 1, [5], N, L, 24, h=h, bc=bc)
+    f = torch.rand(5, N ** 3, dtype=torch.float64, device="cuda")
+    o = torch.empty_like(f)
+    lib, hnd = ctx._lib, ctx.handle
+    dt = 0.9 * h / (L - L / N)
+    n0 = ctx.launch_count()
+    for call, status in (
+        (lambda: lib.fks_set_params(hnd, 0.0, 0.0, 0.0, 1), -1),
+        (lambda: lib.fks_set_params(hnd, -1.0, 0.0, 0.0, 1), -1),
+        (lambda: lib.fks_set_ghost(hnd, 6, ctypes.c_void_p(f.data_ptr())), -1),
+        (lambda: lib.fks_set_ghost(hnd, 0, None), -1),
+        (lambda: lib.fks_set_dirs(hnd, None, None, 0), -1),
+        (lambda: lib.fks_set_state(hnd, -1, dt), -1),
+        (lambda: lib.fks_moments(hnd, ctypes.c_void_p(f.data_ptr()), None, None, None), -1),
+        (lambda: lib.fks_step(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(f.data_ptr()), ctypes.c_double(dt)), -1),
+        (lambda: lib.fks_transport(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(f.data_ptr()), ctypes.c_double(dt)), -1),
+        (lambda: lib.fks_step(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(o.data_ptr()), ctypes.c_double(0.0)), -1),
+        (lambda: lib.fks_step(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(o.data_ptr()), ctypes.c_double(dt)), -7),  # ghost face 0 never set
+    ):
+        assert call() == status, status
+    with pytest.raises(fks.FksError):
+        ctx.set_params(tau=0.0)           # the binding raises on the same status
+    assert ctx.launch_count() == n0
+    ctx.set_ghost(0, f[0].contiguous())
+    ctx.step(f, o, dt)
+    with pytest.raises(fks.FksError) as ei:
+        ctx.step(o, f, 1.5 * dt)          # dt is fixed per run (reading #15)
+    assert ei.value.status == -7
+    n, dt_ = ctx.get_state()
+    assert n == 1 and dt_ == dt
+    ctx.set_state(7, dt)                  # resume: the shifts are pure functions of n
+    ctx.step(o, f, dt)
+    assert ctx.get_state()[0] == 8
+    ctx.check()
