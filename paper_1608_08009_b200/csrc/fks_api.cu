@@ -569,10 +569,11 @@ fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
     e = cudaMemsetAsync(c->d_sync, 0, (size_t)ncl * fks::sync_bytes3d(), c->stream);
     if (e == cudaSuccess) e = fks::launch_step3d(c->N, p, ncl, c->stream);
   } else {
-    const int per = fks::cells_per_block2d(c->N);
+    const bool pair = fks::use_pair2d(c->N, c->A);
+    const int per = pair ? fks::cells_per_block2d_pair(c->N) : fks::cells_per_block2d(c->N);
     const int64_t need = (p.ncells + per - 1) / per;
     const int nb = (int)std::min<int64_t>(need, (int64_t)c->sm_count);
-    e = fks::launch_step2d(c->N, p, nb, c->stream);
+    e = pair ? fks::launch_step2d_pair(c->N, p, nb, c->stream) : fks::launch_step2d(c->N, p, nb, c->stream);
   }
   c->launches++;
   return cuda_fail(e);
@@ -1241,7 +1242,9 @@ static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, doubl
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
   const int64_t n = c->n;
-  const int64_t per_round = c->dv == 3 ? (int64_t)std::max(1, c->nclusters) : (int64_t)c->sm_count * fks::cells_per_block2d(c->N);
+  const int64_t per_round = c->dv == 3 ? (int64_t)std::max(1, c->nclusters)
+                                       : (int64_t)c->sm_count * (fks::use_pair2d(c->N, c->A) ? fks::cells_per_block2d_pair(c->N)
+                                                                                          : fks::cells_per_block2d(c->N));
   int64_t nchunks = 32;  // FKS_HOST_CHUNKS: pipeline depth (C2: 12 chunks 25.6 ms, 32: 24.6 ms; PCIe-bound)
   if (const char* e = getenv("FKS_HOST_CHUNKS")) nchunks = std::max(1, atoi(e));
   int64_t chunk = std::max<int64_t>(per_round * 2, (c->ncells + nchunks - 1) / nchunks);

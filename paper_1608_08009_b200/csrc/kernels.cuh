@@ -16,9 +16,14 @@ size_t sync_bytes3d();
 // 3D table layout: P CTAs per cell, NP l_y planes per CTA, slabr rows (of N entries) per CTA slab.
 int table_layout3d(int N, int* P, int* NP, int* slabr);
 
-// 2D, N = 64 (kernels2d64.cu: pencils split over lane pairs), 2 cells per CTA.
-cudaError_t launch_step2d64(const StepParams& p, int nblocks, cudaStream_t s);
-int cells_per_block2d64();
+// 2D with pencils split over lane pairs (kernels2dp.cu): N = 64 (2 cells per 256-thread CTA) and
+// N = 32 (8 cells per 512-thread CTA, tables in SMEM when (A + 1) directions fit).
+cudaError_t launch_step2d_pair(int N, const StepParams& p, int nblocks, cudaStream_t s);
+int cells_per_block2d_pair(int N);
+bool step2d_pair_fits(int N, int A);
+// Which 2D kernel runs for (N, A): the pair kernel for N = 64 always, for N = 32 when it fits and
+// FKS_2D_PAIR (development knob) does not say otherwise.
+bool use_pair2d(int N, int A);
 
 // 2D (Maxwell molecules): cells_per_block2d(N) cells per CTA.
 cudaError_t launch_step2d(int N, const StepParams& p, int nblocks, cudaStream_t s);

@@ -15,6 +15,8 @@
 // The loss is the (A+1)-th direction with table (D~, 0).  Thread j_y then owns row j_y of Q for
 // the projection (a group reduction of 4 moments) and the Euler update.
 // Folded tables: T[p][l_y][l_x] double2 = (s w_p alpha_p / n, alpha'_p / n); T[A] = (s D / n, 0).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fft.cuh"
 #include "kernels.cuh"
@@ -350,7 +352,6 @@ cudaError_t launch_step2d(int N, const StepParams& p, int nblocks, cudaStream_t 
     case 8: return launch2<8>(p, nblocks, s);
     case 16: return launch2<16>(p, nblocks, s);
     case 32: return launch2<32>(p, nblocks, s);
-    case 64: return launch_step2d64(p, nblocks, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -360,9 +361,15 @@ int cells_per_block2d(int N) {
     case 8: return Cfg2<8>::GROUPS;
     case 16: return Cfg2<16>::GROUPS;
     case 32: return Cfg2<32>::GROUPS;
-    case 64: return cells_per_block2d64();
     default: return 0;
   }
+}
+
+bool use_pair2d(int N, int A) {
+  if (N == 64) return true;
+  if (N != 32 || !step2d_pair_fits(N, A)) return false;
+  const char* e = getenv("FKS_2D_PAIR");
+  return e && atoi(e) == 1;
 }
 
 }  // namespace fks
