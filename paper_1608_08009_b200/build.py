@@ -10,7 +10,8 @@ CSRC = os.path.join(HERE, "csrc")
 # FKS_TIMING=1: the per-phase clock64 instrumentation of kernels3d.cu as libfks_timing.so.
 CHECKED = bool(os.environ.get("FKS_CHECKS"))
 TIMING = bool(os.environ.get("FKS_TIMING"))
-_TAG = "checked" if CHECKED else "timing" if TIMING else None
+# FKS_VARIANT=<tag> (with FKS_NVCC_EXTRA="-D...") builds a named development variant libfks_<tag>.so.
+_TAG = "checked" if CHECKED else "timing" if TIMING else os.environ.get("FKS_VARIANT") or None
 LIB = os.path.join(HERE, f"libfks_{_TAG}.so" if _TAG else "libfks.so")
 OBJDIR = os.path.join(CSRC, _TAG) if _TAG else CSRC
 SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels2dp.cu", "kernels3d.cu", "kernels_aux.cu", "kernels_bgk.cu"]
