@@ -1,5 +1,7 @@
 // HBM-bound companions of the fused step: transport-only (a1+a3), solid-cell copy and the
 // moment reduction (a10).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -49,27 +51,36 @@ __global__ void __launch_bounds__(256) k_transport_cfl1(const double* __restrict
     // k = tid + 256 i: kx = tid % N is loop-invariant (N divides 256); all UNR loads of a batch are
     // issued before its stores (the round-1 loop relied on the compiler for that and lost ~25 % when
     // an unrelated change shifted its register allocation)
-    constexpr int UNR = n >= 2048 ? 8 : (n >= 256 ? n / 256 : 1);  // n / (256 UNR) whole batches
+#ifndef FKS_TR_UNR
+#define FKS_TR_UNR 8
+#endif
+    constexpr int UNR = n >= 256 * FKS_TR_UNR ? FKS_TR_UNR : (n >= 256 ? n / 256 : 1);  // whole batches
     static_assert(n < 256 || n % (256 * UNR) == 0, "whole batches");
     const int kx = threadIdx.x % N;
     const int dx0 = sdelta[0][kx] + 1;
     // few cells (C3: 400 cells for 1184 CTAs): gridDim.y CTAs share a cell, each a range of batches
     const int kspan = n / (int)gridDim.y;
+    auto run = [&](auto reflect) {  // the mirror lookup only exists with specular reflection
 #pragma unroll 1
-    for (int k0 = (int)blockIdx.y * kspan + threadIdx.x; k0 < ((int)blockIdx.y + 1) * kspan; k0 += 256 * UNR) {
-      double v[UNR];
+      for (int k0 = (int)blockIdx.y * kspan + threadIdx.x; k0 < ((int)blockIdx.y + 1) * kspan; k0 += 256 * UNR) {
+        double v[UNR];
 #pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const int k = k0 + 256 * j;
-        const int ky = (k / N) % N, kz = DV == 3 ? k / (N * N) : 0;
-        const int combo = dx0 + 3 * (sdelta[1][ky] + 1) + 9 * (sdelta[2][kz] + 1);
-        const int ks = sflip[combo] ? mirror_k(k, kx, ky, kz, sflip[combo], N) : k;
-        FKS_CHECK(combo >= 0 && combo < 27 && ks >= 0 && ks < n && cell < tp.ncells_total);
-        v[j] = __ldg(sbase[combo] + ks);
+        for (int j = 0; j < UNR; ++j) {
+          const int k = k0 + 256 * j;
+          const int ky = (k / N) % N, kz = DV == 3 ? k / (N * N) : 0;
+          const int combo = dx0 + 3 * (sdelta[1][ky] + 1) + 9 * (sdelta[2][kz] + 1);
+          int ks = k;
+          if constexpr (decltype(reflect)::value)
+            if (sflip[combo]) ks = mirror_k(k, kx, ky, kz, sflip[combo], N);
+          FKS_CHECK(combo >= 0 && combo < 27 && ks >= 0 && ks < n && cell < tp.ncells_total);
+          v[j] = __ldg(sbase[combo] + ks);
+        }
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) out[k0 + 256 * j] = v[j];
       }
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) out[k0 + 256 * j] = v[j];
-    }
+    };
+    if (tp.reflect) run(std::true_type{});
+    else run(std::false_type{});
   }
 }
 
