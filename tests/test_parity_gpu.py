@@ -88,7 +88,7 @@ def test_collide_3d_product_directions(torch, fks):
     assert rel_err_Q(host(Q), f, tab, direct=True) <= TOL
 
 
-@pytest.mark.parametrize("kind", ["smooth", "random"])
+@pytest.mark.parametrize("kind", ["smooth", "random", "neareq"])
 def test_collide_3d_32(torch, fks, kind):
     """N = 32^3, 24-design (C2 shape), more cells than resident clusters (ragged tail)."""
     N, L = 32, 7.0

@@ -313,3 +313,47 @@ def test_configuration_and_state_errors(torch, fks):
     ctx.step(o, f, dt)
     assert ctx.get_state()[0] == 8
     ctx.check()
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_full_size_256_cells(torch, fks, name):
+    """§8(c.5) evaluator rule: at least 256 sampled cells per 3D config against the oracle's cpu_fft
+    (C3: all 400 cells), one fused step at full size in bench.py's launch configuration."""
+    c = workloads.config(name)
+    N, L, A, dv, dxd = c["N"], c["L"], c["A"], c["dv"], c["dx_dim"]
+    tab = tables.build_tables(dv, N, L)
+    rng = np.random.default_rng(256)
+    if dxd == 0:
+        nc = c["cells"][0]
+        f = workloads.initial_state(c)
+        ctx = fks.Context(dv, 0, [nc], N, L, A)
+        fin = dev(torch, f)
+        out = torch.empty_like(fin)
+        ctx.step(fin, out, c["dt"])
+        ctx.check()
+        sample = sorted(rng.choice(nc, size=256, replace=False).tolist())
+        got = host(out[sample])
+        ref = ostep.homogeneous_step(f[sample], tab, c["dt"], c["tau"])
+        for i in range(256):
+            assert np.max(np.abs(got[i] - ref[i])) <= TOL * np.max(np.abs(ref[i])), sample[i]
+        return
+    M = list(c["cells"][::-1])
+    nc = int(np.prod(M))
+    Fd, Fh = _scaled_state(torch, c, seed=256)
+    ghosts = workloads.ghost_vectors(c)
+    solid = workloads.solid_mask(c)
+    ctx = fks.Context(dv, dxd, M, N, L, A, h=c["dx"], bc=c["bc"])
+    for face, g in ghosts.items():
+        ctx.set_ghost(face, dev(torch, g))
+    if solid is not None:
+        ctx.set_solid(solid)
+    ctx.set_params(tau=c["tau"])
+    out = torch.empty_like(Fd)
+    ctx.step(Fd, out, c["dt"])
+    ctx.check()
+    sample = list(range(nc)) if nc <= 400 else sorted(rng.choice(nc, size=256, replace=False).tolist())
+    got = host(out[sample]).reshape((-1,) + (N,) * dv)
+    del out, Fd
+    torch.cuda.empty_cache()
+    fstar = transport.gather(Fh, 0, dxd, dv, N, L, c["dt"], c["dx"], c["bc"], ghosts, cells=sample)
+    _check_sampled(got, sample, fstar, None if solid is None else solid.reshape(-1), Fh, c, tab)
