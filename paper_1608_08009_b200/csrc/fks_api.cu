@@ -1372,6 +1372,7 @@ fks_status fks_finalize(fks_ctx* c) {
   cudaFree(c->d_host_out);
   cudaFree(c->d_tmp);
   if (c->nccl) {
+    if (c->s_comm) cudaStreamSynchronize(c->s_comm);  // no exchange in flight when the comm goes
     if (const NcclApi* nc = nccl_api()) nc->commDestroy(c->nccl);
   }
   if (c->loop)
