@@ -182,10 +182,12 @@ fks_status fks_transport(fks_ctx* ctx, const double* f_in, double* f_out, double
 fks_status fks_step(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
 
 /* fks_step with HOST buffers: copies f_in_host to the device, steps, copies the result back
- * to f_out_host and synchronises (end-to-end path; pinned memory recommended).  For independent
- * cells (dx = 0, no solids) the batch is processed in chunks so that the host->device copy, the
- * step and the device->host copy of consecutive chunks overlap (two library-owned copy
- * streams); the result is bitwise that of fks_step. */
+ * to f_out_host and synchronises (end-to-end path; pinned memory recommended).  The batch is
+ * processed in chunks so that the host->device copy, the step and the device->host copy of
+ * consecutive chunks overlap (two library-owned copy streams): cells for dx = 0 without solids,
+ * planes of the slowest axis for dx > 0 (a chunk steps once the next chunk's first plane landed;
+ * not with a periodic or HALO slab axis, a comm, CFL > 1 along it, or a non-default scheme, which
+ * take the one-shot path).  The result is bitwise that of fks_step. */
 fks_status fks_step_host(fks_ctx* ctx, const double* f_in_host, double* f_out_host, double dt);
 
 /* NEXT-2 (beyond the Boltzmann hot path): one BGK step, F = f* + (dt/tau) nu (E[f*] - f*), with

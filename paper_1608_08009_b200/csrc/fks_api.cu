@@ -372,6 +372,10 @@ struct fks_ctx {
   std::vector<uint8_t> h_solid;    // host copy of the solid mask (empty: none)
   uint8_t* d_halo_solid[2] = {nullptr, nullptr};  // neighbour planes' solid flags (specular + comm)
   uint8_t* d_zero_mask = nullptr;  // all-fluid mask / plane for contexts without solids (specular)
+  // fks_step_host on a spatial grid: per plane-chunk fluid / solid cell lists (built on first use)
+  std::vector<int64_t> chunk_first;  // first plane of each chunk (+ the end)
+  std::vector<int*> d_chunk_fluid, d_chunk_solid;
+  std::vector<int> n_chunk_fluid, n_chunk_solid;
 };
 
 // Loopback communicator: contexts of one process (one device) exchange through device copies,
@@ -450,7 +454,18 @@ void build_gram(fks_ctx* c) {
 
 fks_status update_comm_lists(fks_ctx* c);
 
+void free_chunk_lists(fks_ctx* c) {
+  for (int* p : c->d_chunk_fluid) cudaFree(p);
+  for (int* p : c->d_chunk_solid) cudaFree(p);
+  c->d_chunk_fluid.clear();
+  c->d_chunk_solid.clear();
+  c->n_chunk_fluid.clear();
+  c->n_chunk_solid.clear();
+  c->chunk_first.clear();
+}
+
 fks_status set_cell_lists(fks_ctx* c, const uint8_t* solid_host) {
+  free_chunk_lists(c);
   if (solid_host) c->h_solid.assign(solid_host, solid_host + c->ncells);
   else c->h_solid.clear();
   std::vector<int> fluid, solid;
@@ -1295,6 +1310,104 @@ static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, doubl
   return cuda_fail(cudaStreamSynchronize(c->stream));
 }
 
+// fks_step_host on a spatial grid (dx > 0): the grid is cut into chunks of planes along the slowest
+// axis; chunk i's step needs its own planes and the first plane of chunk i+1 (shifts of one cell at
+// CFL <= 1), so it starts as soon as those host->device copies landed, and its device->host copy
+// overlaps the following chunks' copies and steps.  Bitwise the one-shot path (same kernels per
+// cell).  Falls back when the slab axis is periodic or a HALO face (the first chunk would need the
+// last), with a comm, with CFL > 1 along the slab axis, or with a non-default time scheme.
+static fks_status step_host_spatial(fks_ctx* c, const double* f_in_host, double* f_out_host, double dt, bool* done) {
+  *done = false;
+  const int a = c->grid.dx - 1;
+  const int64_t Ma = c->grid.M[a];
+  const int64_t pc = c->ncells / Ma;
+  if (c->grid.bc[2 * a] == FKS_BC_PERIODIC || c->grid.bc[2 * a + 1] == FKS_BC_PERIODIC ||
+      c->grid.bc[2 * a] == FKS_BC_HALO || c->grid.bc[2 * a + 1] == FKS_BC_HALO || c->comm_kind ||
+      c->integ != FKS_TIME_EULER || c->split != FKS_SPLIT_LIE || Ma < 4)
+    return FKS_OK;
+  fks_status st = check_dt(c, dt);
+  if (st != FKS_OK) return st;
+  fks::StepParams p = base_params(c, c->d_host_in, c->d_host_out, 1);
+  if ((st = fill_transport(c, &p.tp, true)) != FKS_OK) return st;
+  for (int k = 0; k < c->N; ++k)
+    if (p.tp.delta[a][k] < -1 || p.tp.delta[a][k] > 1) return FKS_OK;  // needs more than one neighbour plane
+  if (c->chunk_first.empty()) {  // chunk lists (fluid / solid cells per chunk of planes)
+    const int64_t nch = std::min<int64_t>(16, Ma / 2);
+    for (int64_t i = 0; i <= nch; ++i) c->chunk_first.push_back(Ma * i / nch);
+    for (int64_t i = 0; i < nch; ++i) {
+      std::vector<int> fl, so;
+      for (int64_t cell = c->chunk_first[i] * pc; cell < c->chunk_first[i + 1] * pc; ++cell)
+        ((!c->h_solid.empty() && c->h_solid[cell]) ? so : fl).push_back((int)cell);
+      int *dfl = nullptr, *dso = nullptr;
+      if (!fl.empty()) {
+        if (cudaMalloc(&dfl, fl.size() * sizeof(int)) != cudaSuccess) return FKS_E_NOMEM;
+        cudaMemcpy(dfl, fl.data(), fl.size() * sizeof(int), cudaMemcpyHostToDevice);
+      }
+      if (!so.empty()) {
+        if (cudaMalloc(&dso, so.size() * sizeof(int)) != cudaSuccess) return FKS_E_NOMEM;
+        cudaMemcpy(dso, so.data(), so.size() * sizeof(int), cudaMemcpyHostToDevice);
+      }
+      c->d_chunk_fluid.push_back(dfl);
+      c->d_chunk_solid.push_back(dso);
+      c->n_chunk_fluid.push_back((int)fl.size());
+      c->n_chunk_solid.push_back((int)so.size());
+    }
+  }
+  const int nch = (int)c->chunk_first.size() - 1;
+  if (!c->s_h2d) {
+    if (cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+      return FKS_E_CUDA;
+  }
+  while ((int)c->ev_in.size() < nch) {
+    cudaEvent_t e1, e2;
+    if (cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
+      return FKS_E_CUDA;
+    c->ev_in.push_back(e1);
+    c->ev_out.push_back(e2);
+  }
+  cudaEvent_t start;
+  if (cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess) return FKS_E_CUDA;
+  cudaEventRecord(start, c->stream);
+  cudaStreamWaitEvent(c->s_h2d, start, 0);
+  cudaStreamWaitEvent(c->s_d2h, start, 0);
+  const int64_t n = c->n;
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < nch && e == cudaSuccess; ++i) {  // all copies in, chunk by chunk
+    const int64_t off = c->chunk_first[i] * pc * n, cnt = (c->chunk_first[i + 1] - c->chunk_first[i]) * pc * n;
+    e = cudaMemcpyAsync(c->d_host_in + off, f_in_host + off, (size_t)cnt * sizeof(double), cudaMemcpyHostToDevice,
+                        c->s_h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_in[i], c->s_h2d);
+  }
+  for (int i = 0; i < nch && e == cudaSuccess && st == FKS_OK; ++i) {
+    // chunk i reads its planes and the first plane of chunk i + 1
+    e = cudaStreamWaitEvent(c->stream, c->ev_in[std::min(i + 1, nch - 1)], 0);
+    if (e == cudaSuccess && c->n_chunk_solid[i]) {
+      e = fks::launch_copy_cells(c->d_host_in, c->d_host_out, c->d_chunk_solid[i], c->n_chunk_solid[i], c->n, c->stream);
+      c->launches++;
+    }
+    if (e != cudaSuccess) break;
+    p.cell_list = c->d_chunk_fluid[i];
+    p.ncells = c->n_chunk_fluid[i];
+    st = run_collision(c, p);
+    if (st != FKS_OK) break;
+    const int64_t off = c->chunk_first[i] * pc * n, cnt = (c->chunk_first[i + 1] - c->chunk_first[i]) * pc * n;
+    e = cudaEventRecord(c->ev_out[i], c->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_d2h, c->ev_out[i], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(f_out_host + off, c->d_host_out + off, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                          c->s_d2h);
+  }
+  cudaEventDestroy(start);
+  if (st != FKS_OK) return st;
+  if (e != cudaSuccess) return FKS_E_CUDA;
+  c->step_n++;
+  *done = true;
+  if (cudaStreamSynchronize(c->s_d2h) != cudaSuccess) return FKS_E_CUDA;
+  return cuda_fail(cudaStreamSynchronize(c->stream));
+}
+
 fks_status fks_step_host(fks_ctx* c, const double* f_in_host, double* f_out_host, double dt) {
   if (!c || !f_in_host || !f_out_host) return FKS_E_INVAL;
   const size_t bytes = (size_t)c->ncells * c->n * sizeof(double);
@@ -1310,6 +1423,11 @@ fks_status fks_step_host(fks_ctx* c, const double* f_in_host, double* f_out_host
   }
   if (c->grid.dx == 0 && c->nsolid == 0 && c->integ == FKS_TIME_EULER)
     return step_host_pipelined(c, f_in_host, f_out_host, dt);
+  if (c->grid.dx > 0) {
+    bool done = false;
+    fks_status st = step_host_spatial(c, f_in_host, f_out_host, dt, &done);
+    if (st != FKS_OK || done) return st;
+  }
   if (cudaMemcpyAsync(c->d_host_in, f_in_host, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     return FKS_E_CUDA;
   fks_status st = fks_step(c, c->d_host_in, c->d_host_out, dt);
@@ -1385,6 +1503,7 @@ fks_status fks_finalize(fks_ctx* c) {
   }
   cudaFree(c->d_interior);
   cudaFree(c->d_boundary);
+  free_chunk_lists(c);
   cudaFree(c->d_halo_solid[0]);
   cudaFree(c->d_halo_solid[1]);
   cudaFree(c->d_zero_mask);
