@@ -6,6 +6,7 @@ O=gpurun_out/final
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "exit $?" >> $O/smoke.log
+FKS_LIB_VARIANT=checked timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu_checked.log 2>&1; echo "exit $?" >> $O/pytest_gpu_checked.log
 python bench.py > $O/bench_C2.json 2> $O/bench_C2.err
 for cfg in C1 C3 C4 C5; do
   python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_$cfg.json 2> $O/bench_$cfg.err
