@@ -14,8 +14,9 @@ TIMING = bool(os.environ.get("FKS_TIMING"))
 _TAG = "checked" if CHECKED else "timing" if TIMING else os.environ.get("FKS_VARIANT") or None
 LIB = os.path.join(HERE, f"libfks_{_TAG}.so" if _TAG else "libfks.so")
 OBJDIR = os.path.join(CSRC, _TAG) if _TAG else CSRC
-SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels2dp.cu", "kernels3d.cu", "kernels_aux.cu", "kernels_bgk.cu"]
-HEADERS = ["fft.cuh", "common.cuh", "kernels.cuh", os.path.join("..", "..", "include", "fks.h")]
+SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels2dp.cu", "kernels3d.cu", "kernels3d64.cu", "kernels_aux.cu",
+           "kernels_bgk.cu"]
+HEADERS = ["fft.cuh", "fftp.cuh", "common.cuh", "kernels.cuh", os.path.join("..", "..", "include", "fks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + (["-DFKS_CHECKS"] if CHECKED else []) + os.environ.get("FKS_NVCC_EXTRA", "").split() + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v",

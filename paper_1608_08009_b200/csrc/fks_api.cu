@@ -400,7 +400,7 @@ fks_status upload_tables(fks_ctx* c) {
                  : make_double2(s * D[k] / n, 0.0);
   };
   std::vector<double2> T;
-  if (c->dv == 2) {  // T[p][l_y][l_x]
+  if (c->dv == 2 || N == 64) {  // T[p][k], k = l_x + N l_y (+ N^2 l_z)
     T.resize((size_t)(A + 1) * n);
     for (int p = 0; p <= A; ++p)
       for (int k = 0; k < n; ++k) T[(size_t)p * n + k] = folded(p, k);
@@ -579,7 +579,11 @@ fks::StepParams base_params(fks_ctx* c, const double* f_in, double* f_out, int m
 fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
   if (p.ncells == 0) return FKS_OK;
   cudaError_t e;
-  if (c->dv == 3) {
+  if (c->dv == 3 && c->N == 64) {
+    const int ncl = std::min<int64_t>(p.ncells, c->nclusters);
+    e = cudaMemsetAsync(c->d_sync, 0, (size_t)ncl * fks::sync_bytes3d64(), c->stream);
+    if (e == cudaSuccess) e = fks::launch_step3d64(p, ncl, c->stream);
+  } else if (c->dv == 3) {
     const int ncl = std::min<int64_t>(p.ncells, c->nclusters);
     e = cudaMemsetAsync(c->d_sync, 0, (size_t)ncl * fks::sync_bytes3d(), c->stream);
     if (e == cudaSuccess) e = fks::launch_step3d(c->N, p, ncl, c->stream);
@@ -594,9 +598,9 @@ fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
   return cuda_fail(e);
 }
 
-// Velocity nodes per axis: 8, 16, 32 in 2D and 3D, 64 in 2D (P:624-625 quotes 16-64 per axis; the
-// 3D 64^3 transform, 4 MiB per complex field, exceeds the 8-SM group design -- DESIGN.md §10).
-bool valid_N(int N, int dv) { return N == 8 || N == 16 || N == 32 || (N == 64 && dv == 2); }
+// Velocity nodes per axis: 8, 16, 32, 64 in 2D and 3D (P:624-625 quotes 16-64 per axis; 3D N = 64
+// runs kernels3d64.cu, a 64-CTA group per cell).
+bool valid_N(int N, int dv) { (void)dv; return N == 8 || N == 16 || N == 32 || N == 64; }
 
 }  // namespace
 
@@ -916,15 +920,17 @@ fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double k
     else cudaMemset(c->d_flag, 0, sizeof(int));
   }
   if (st == FKS_OK && dv == 3) {
-    c->nclusters = fks::max_active_clusters3d(Nv);
+    c->nclusters = Nv == 64 ? fks::max_groups3d64() : fks::max_active_clusters3d(Nv);
     if (const char* e = getenv("FKS_MAX_CLUSTERS")) {  // development: scaling with the cluster count
       const int m = atoi(e);
       if (m > 0 && m < c->nclusters) c->nclusters = m;
     }
     if (getenv("FKS_VERBOSE")) fprintf(stderr, "fks: N=%d, %d resident CTA groups\n", Nv, c->nclusters);
     if (c->nclusters <= 0) st = FKS_E_CUDA;
-    else if (cudaMalloc(&c->d_scratch, (size_t)c->nclusters * fks::scratch_elems3d(Nv) * sizeof(double2)) != cudaSuccess ||
-             cudaMalloc(&c->d_sync, (size_t)c->nclusters * fks::sync_bytes3d()) != cudaSuccess)
+    else if (cudaMalloc(&c->d_scratch, (size_t)c->nclusters * (Nv == 64 ? fks::scratch_elems3d64() : fks::scratch_elems3d(Nv)) *
+                                           sizeof(double2)) != cudaSuccess ||
+             cudaMalloc(&c->d_sync, (size_t)c->nclusters * (Nv == 64 ? fks::sync_bytes3d64() : fks::sync_bytes3d())) !=
+                 cudaSuccess)
       st = FKS_E_NOMEM;
   }
   if (st == FKS_OK) st = set_cell_lists(c, nullptr);

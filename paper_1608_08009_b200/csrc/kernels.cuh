@@ -16,6 +16,14 @@ size_t sync_bytes3d();
 // 3D table layout: P CTAs per cell, NP l_y planes per CTA, slabr rows (of N entries) per CTA slab.
 int table_layout3d(int N, int* P, int* NP, int* slabr);
 
+// 3D, N = 64 (kernels3d64.cu): a group of 64 co-resident CTAs per cell (cooperative launch, two
+// CTAs per SM); scratch = ngroups * scratch_elems3d64() double2, sync = ngroups * sync_bytes3d64()
+// bytes, zeroed before every launch.  Tables in the full layout T[p][n].
+cudaError_t launch_step3d64(const StepParams& p, int ngroups, cudaStream_t s);
+int max_groups3d64();
+size_t scratch_elems3d64();
+size_t sync_bytes3d64();
+
 // 2D with pencils split over lane pairs (kernels2dp.cu): N = 64 (2 cells per 256-thread CTA) and
 // N = 32 (8 cells per 512-thread CTA, tables in SMEM when (A + 1) directions fit).
 cudaError_t launch_step2d_pair(int N, const StepParams& p, int nblocks, cudaStream_t s);

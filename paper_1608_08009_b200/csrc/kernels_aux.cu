@@ -99,7 +99,7 @@ cudaError_t launch_transport(const double* f_in, double* f_out, const TransportP
     while (n >= 2048 * 2 * ky && (int64_t)nb * ky * 2 <= (int64_t)sms * 8 && ky < 16) ky *= 2;
 #define FKS_TR(NN, DD) \
   if (N == NN && dv == DD) { k_transport_cfl1<NN, DD><<<dim3(nb, ky), 256, 0, s>>>(f_in, f_out, tp, solid, ncells); return cudaGetLastError(); }
-    FKS_TR(8, 2) FKS_TR(16, 2) FKS_TR(32, 2) FKS_TR(64, 2) FKS_TR(8, 3) FKS_TR(16, 3) FKS_TR(32, 3)
+    FKS_TR(8, 2) FKS_TR(16, 2) FKS_TR(32, 2) FKS_TR(64, 2) FKS_TR(8, 3) FKS_TR(16, 3) FKS_TR(32, 3) FKS_TR(64, 3)
 #undef FKS_TR
   }
   const int threads = 256;
@@ -264,7 +264,7 @@ cudaError_t launch_moments(const double* f, double* rho, double* u, double* T, i
   }
 #define FKS_MO(NN, DD) \
   if (N == NN && dv == DD) { k_moments<NN, DD><<<nb, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
-  FKS_MO(8, 2) FKS_MO(16, 2) FKS_MO(32, 2) FKS_MO(8, 3) FKS_MO(16, 3) FKS_MO(32, 3)
+  FKS_MO(8, 2) FKS_MO(16, 2) FKS_MO(32, 2) FKS_MO(8, 3) FKS_MO(16, 3) FKS_MO(32, 3) FKS_MO(64, 3)
 #undef FKS_MO
   return cudaErrorInvalidValue;
 }
