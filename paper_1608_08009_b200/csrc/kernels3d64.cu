@@ -13,10 +13,15 @@
 // transform (a4) runs the same passes in the other order: plane FFT along x then y (F1), barrier,
 // pencil FFT along z into TMEM (F2).  Two exchange buffers alternate, so one barrier per item
 // suffices: a CTA writing item t + 2 has passed barrier t + 1, which every CTA reaches only after
-// reading item t.
+// reading item t.  (Software-pipelining the next direction's pencils into the barrier wait, with
+// a ring of four buffers, measured slower: 10.45 vs 10.0 ms per 128-cell step.)
 // Every 64-point pencil is split over a lane pair (fftp.cuh): 128 threads = 64 pencils, two CTAs
-// (two different groups) per SM.  Tables: full layout T[p][l_z][l_y][l_x], pre-folded as in
+// (two different groups) per SM, all CTAs co-resident (launch_step3d64).  Tables: full layout T[p][l_z][l_y][l_x], pre-folded as in
 // kernels3d.cu (alpha~ = s w_p alpha_p / n, alpha'~ = alpha'_p / n, D~ = s D / n).
+#include <cstdio>
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fft.cuh"
 #include "fftp.cuh"
@@ -32,7 +37,12 @@ constexpr int PL64 = N64 * N64;          // plane
 constexpr int NN64 = N64 * N64 * N64;    // one cell
 constexpr int P64 = 64;                  // CTAs per cell: one j_z plane / one l_y pencil plane each
 constexpr int T64 = 128;                 // threads per CTA: one lane pair per pencil
-constexpr int TMEM64 = 256;              // f^ (32 complex = 128 columns) + f* (32 fp64 = 64 columns)
+#ifndef FKS_N64_CTAS
+#define FKS_N64_CTAS 2
+#endif
+constexpr int CTAS64 = FKS_N64_CTAS;     // resident CTAs per SM (2, or 3 with f* re-gathered)
+constexpr bool FS_TMEM64 = CTAS64 == 2;  // f* cached in TMEM for the loss term and the update
+constexpr int TMEM64 = FS_TMEM64 ? 256 : 128;  // f^ (32 complex = 128 columns) [+ f* (32 fp64 = 64 columns)]
 
 // Group barrier counter and the projection partials of one group (zeroed before every launch).
 struct Sync64 {
@@ -47,8 +57,10 @@ constexpr size_t OFF_TMEM64 = OFF_RED64 + 25 * 8;
 constexpr size_t SMEM_USED64 = OFF_TMEM64 + 16;
 // Requested dynamic SMEM: large enough that a third CTA never fits an SM -- its tcgen05.alloc would
 // wait for columns held by the two resident CTAs of other groups while its own group waits for it.
-constexpr size_t SMEM64 = 100 * 1024;
-static_assert(SMEM_USED64 <= SMEM64 && 3 * (SMEM64 + 1024) > 233472 && 2 * (SMEM64 + 1024) <= 233472, "2 CTAs per SM");
+constexpr size_t SMEM64 = CTAS64 == 2 ? 100 * 1024 : 72 * 1024;
+static_assert(SMEM_USED64 <= SMEM64 && (CTAS64 + 1) * (SMEM64 + 1024) > 233472 &&
+                  CTAS64 * (SMEM64 + 1024) <= 233472 && CTAS64 * TMEM64 <= 512,
+              "CTAS64 CTAs per SM, never one more");
 
 // Element (row r, column c) of the SMEM plane.  XOR swizzle on the 16-byte slots within 128 B:
 // bits 1-2 from r & 3 (row sweeps: 4 rows x 2 parities per quarter warp) and bit 2 from r >> 5
@@ -105,7 +117,7 @@ __device__ __forceinline__ void group_bar(Sync64* gs, unsigned& target) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
+__global__ void __launch_bounds__(T64, CTAS64) k_step3d64(const StepParams p) {
   constexpr int N = N64, H = H64, n = NN64, PL = PL64;
   extern __shared__ __align__(128) unsigned char smem[];
   double2* pl = reinterpret_cast<double2*>(smem);  // one 64 x 64 complex plane (sw64)
@@ -131,13 +143,19 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
   FKS_CHECK((tbase & 0xffffu) + TMEM64 <= 512u);
   const uint32_t faddr = tbase + ((uint32_t)(32 * w) << 16);  // f^ of pencil (q, rank), l_z = 2m + h
   const uint32_t saddr = faddr + 128;                          // f*(x = H h + j, y = q, z = rank)
-  unsigned target = 0;  // group barrier count x P64
+  unsigned target = 0;  // group barriers so far x P64
   unsigned item = 0;    // exchange items so far (buffer item & 1)
 
   for (int it = grp; it < p.ncells; it += ngrp) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
     FKS_CHECK(cell >= 0 && cell < p.tp.ncells_total);
     const CellCoord cc = cell_coord(p.tp, cell);
+    // f*(x = H h + j, y = q, z = rank) when it is not cached in TMEM: gathered again (a3)
+    auto fstar_at = [&](int j) -> double {
+      const int x = H * h + j;
+      if (p.tp.dx == 0) return __ldg(p.f_in + cell * (int64_t)n + PL * rank + N * q + x);
+      return gather_fstar(p.f_in, p.tp, cc, x + N * (q + N * rank), x, q, rank, n, sdelta);
+    };
     __syncthreads();  // plane / red free (previous cell)
     {  // F1 (a3 + a4): row y = q of plane z = rank: f* halves (cached in TMEM), DIF along x
       double2 r[H];
@@ -156,15 +174,17 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
           r[j] = make_double2(gather_fstar(p.f_in, p.tp, cc, x + N * (q + N * rank), x, q, rank, n, sdelta), 0.0);
         }
       }
+      if constexpr (FS_TMEM64) {
 #pragma unroll
-      for (int ch = 0; ch < H / 16; ++ch) {
-        uint32_t v[32];
+        for (int ch = 0; ch < H / 16; ++ch) {
+          uint32_t v[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          v[2 * i] = __double2loint(r[ch * 16 + i].x);
-          v[2 * i + 1] = __double2hiint(r[ch * 16 + i].x);
+          for (int i = 0; i < 16; ++i) {
+            v[2 * i] = __double2loint(r[ch * 16 + i].x);
+            v[2 * i + 1] = __double2hiint(r[ch * 16 + i].x);
+          }
+          tm_st32(saddr + ch * 32, v);
         }
-        tm_st32(saddr + ch * 32, v);
       }
       fftp_dif<N, -1>(r, h);
 #pragma unroll
@@ -209,17 +229,21 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
     for (int d = 0; d <= p.A; ++d) {
       double2* wb = wbuf + (size_t)(item & 1) * n;
       {  // I1: X = T f^ on pencil (q, rank), DIT IFFT along z -> exchange [j_z = H h + j][rank][q]
+        // the next direction's table rows of this pencil plane -> L2 (read-only, one item ahead)
+        if (d < p.A && t < N)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.tables + (size_t)(d + 1) * n +
+                                                                            (size_t)t * PL + (size_t)rank * N),
+                       "r"((uint32_t)(N * sizeof(double2)))
+                       : "memory");
         double2 c[H];
         const double2* td = p.tables + (size_t)d * n + (size_t)rank * N + q;
 #pragma unroll
-        for (int ch = 0; ch < H / 8; ++ch) {
-          double2 tt[8];
+        for (int m = 0; m < H; ++m) {  // all 32 table loads in flight (l_z = 2m + h)
+          FKS_CHECK((int64_t)d * n + (int64_t)(2 * m + h) * PL + rank * N + q < p.table_elems);
+          c[m] = __ldg(td + (size_t)(2 * m + h) * PL);
+        }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int lz = 2 * (ch * 8 + i) + h;
-            FKS_CHECK((int64_t)d * n + (int64_t)lz * PL + rank * N + q < p.table_elems);
-            tt[i] = __ldg(td + (size_t)lz * PL);
-          }
+        for (int ch = 0; ch < H / 8; ++ch) {
           uint32_t v[32];
           tm_ld32(faddr + ch * 32, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
@@ -227,7 +251,8 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
           for (int i = 0; i < 8; ++i) {
             const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
             const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
-            c[ch * 8 + i] = make_double2(fma(tt[i].x, Fx, -tt[i].y * Fy), fma(tt[i].x, Fy, tt[i].y * Fx));
+            const double2 tt = c[ch * 8 + i];
+            c[ch * 8 + i] = make_double2(fma(tt.x, Fx, -tt.y * Fy), fma(tt.x, Fy, tt.y * Fx));
           }
         }
         fftp_dit<N, +1>(c, h);
@@ -254,7 +279,7 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
         if (d < p.A) {
 #pragma unroll
           for (int j = 0; j < H; ++j) gacc[j] = fma(r[j].x, r[j].y, gacc[j]);
-        } else {
+        } else if constexpr (FS_TMEM64) {
 #pragma unroll
           for (int ch = 0; ch < H / 16; ++ch) {
             uint32_t v[32];
@@ -266,6 +291,9 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
               gacc[ch * 16 + i] = gacc[ch * 16 + i] - fs * r[ch * 16 + i].x;  // Q = G - f* c
             }
           }
+        } else {
+#pragma unroll
+          for (int j = 0; j < H; ++j) gacc[j] = gacc[j] - fstar_at(j) * r[j].x;
         }
       }
       ++item;
@@ -325,12 +353,14 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
 #pragma unroll
     for (int ch = 0; ch < H / 16; ++ch) {
       uint32_t v[32];
-      tm_ld32(saddr + ch * 32, v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if constexpr (FS_TMEM64) {
+        tm_ld32(saddr + ch * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int j = ch * 16 + i;
-        const double fs = __hiloint2double(v[2 * i + 1], v[2 * i]);
+        const double fs = FS_TMEM64 ? __hiloint2double(v[2 * i + 1], v[2 * i]) : fstar_at(j);
         const double vx = node_v(H * h + j, p.L, p.dv);
         const double corr = lam[0] + lam[1] * vx + lam[2] * vy + lam[3] * vz + lam[4] * (vx * vx + vy * vy + vz * vz);
         double o = fma(p.dt_tau, gacc[j] - corr, fs);
@@ -346,34 +376,47 @@ __global__ void __launch_bounds__(T64, 2) k_step3d64(const StepParams p) {
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(TMEM64) : "memory");
 }
 
-// Cooperative launch: the group barriers need all P64 * ngroups CTAs co-resident.
-cudaError_t launch_step3d64(const StepParams& p, int ngroups, cudaStream_t s) {
+// The full shared-memory carveout for CTAS64 CTAs per SM.
+static cudaError_t prep64() {
   cudaError_t e = cudaFuncSetAttribute(k_step3d64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM64);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_step3d64, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  return e;
+}
+
+// A plain launch of at most CTAS64 CTAs per SM, all co-resident: the group barriers need every
+// CTA of a group running.  Not a cooperative launch: the runtime's occupancy calculation answers
+// one CTA per SM for this kernel whatever its registers / shared memory / block size (apparently
+// assuming a TMEM-allocating kernel owns the SM's 512 columns), although two CTAs of 256 columns
+// each run side by side (measured: 10.1 vs 15.7 ms per 128-cell step; profiles/r02_n64.md).
+// max_groups3d64 counts the slots from the register file and shared memory itself; with nothing
+// else on the device every CTA of the grid is resident at once, and a group barrier that is
+// never completed traps after ~2^24 polls instead of hanging.
+cudaError_t launch_step3d64(const StepParams& p, int ngroups, cudaStream_t s) {
+  cudaError_t e = prep64();
   if (e != cudaSuccess) return e;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ngroups * P64);
-  cfg.blockDim = dim3(T64);
-  cfg.dynamicSmemBytes = SMEM64;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_step3d64, p);
+  k_step3d64<<<ngroups * P64, T64, SMEM64, s>>>(p);
+  return cudaGetLastError();
 }
 
 int max_groups3d64() {
-  if (cudaFuncSetAttribute(k_step3d64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM64) != cudaSuccess)
-    return 0;
-  int per_sm = 0, dev = 0, sms = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step3d64, T64, SMEM64) != cudaSuccess) return 0;
-  if (per_sm > 512 / TMEM64) per_sm = 512 / TMEM64;  // TMEM columns per SM
-  cudaGetDevice(&dev);
+  if (prep64() != cudaSuccess) return 0;
+  cudaFuncAttributes fa;
+  int dev = 0, sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
+  if (cudaFuncGetAttributes(&fa, k_step3d64) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess) return 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  const int regs_cta = (fa.numRegs + 7) / 8 * 8 * T64;  // 8-register allocation granularity
+  int per_sm = CTAS64;
+  per_sm = std::min(per_sm, regs_sm / regs_cta);
+  per_sm = std::min(per_sm, smem_sm / (int)(SMEM64 + fa.sharedSizeBytes + smem_rsv));
+  if (getenv("FKS_VERBOSE"))
+    fprintf(stderr, "fks: k_step3d64 %d CTAs per SM x %d SMs (%d registers, %zu B SMEM per CTA)\n", per_sm, sms,
+            fa.numRegs, SMEM64);
   return per_sm * sms / P64;
 }
-
 size_t scratch_elems3d64() { return (size_t)2 * NN64; }
 
 size_t sync_bytes3d64() { return sizeof(Sync64); }
