@@ -92,6 +92,7 @@ P, G_, O = transport.PERIODIC, transport.GHOST, transport.OUTFLOW
     (2, 2, [5, 6], 16, [P, P, P, P], 3, None),
     (3, 3, [3, 2, 5], 8, [O, O, P, P, G_, O], 2, 7),
     (3, 3, [3, 3, 8], 8, [G_, O, O, O, P, P], 4, 20),    # ring of 4 along z
+    (1, 3, [5], 64, [G_, O], 2, 2),                       # 64^3 (k_step3d64)
 ])
 def test_loopback_step_bitwise(torch, fks, dxd, dv, M, N, bc, world, solid_at):
     L = 6.0

@@ -162,6 +162,8 @@ def test_C4_geometry_specular_n32(torch, fks):
 @pytest.mark.parametrize("dxd,dv,M,N,bc,solid_cell", [
     (1, 3, [40], 8, [transport.GHOST, transport.GHOST], None),
     (2, 2, [9, 7], 16, [transport.GHOST, transport.OUTFLOW, transport.OUTFLOW, transport.OUTFLOW], 20),
+    (1, 3, [6], 64, [transport.GHOST, transport.OUTFLOW], 3),
+    (0, 3, [9], 64, [], None),                           # homogeneous: the pipelined host path
 ])
 def test_step_host_spatial(torch, fks, dxd, dv, M, N, bc, solid_cell):
     """fks_step_host (host buffers, one H2D + step + D2H) on spatial grids equals fks_step bitwise."""
