@@ -170,15 +170,19 @@ fks_status fks_set_scheme(fks_ctx* ctx, int splitting, int integrator);
 fks_status fks_set_stream(fks_ctx* ctx, void* cuda_stream);
 
 /* a4-a7: Q[cell][k] = Q(f[cell]) for every local cell, unprojected, user units, no 1/tau.
- * f and Q must not overlap. */
+ * In-place calls: here and in fks_transport / fks_step / fks_step_bgk the output
+ * may be the input pointer itself -- the result then goes to a library-owned state-sized buffer
+ * (allocated on first use) and one device-to-device copy on the context stream moves it back.
+ * Partially overlapping buffers are invalid (not detected). */
 fks_status fks_collide(fks_ctx* ctx, const double* f, double* Q);
 
 /* a1 + a3: f_out = transported f_in for the step n -> n+1, then n += 1 (collision skipped).
  * dt must equal the context dt once one was set (it is fixed per run, reading #15). */
 fks_status fks_transport(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
 
-/* a1..a9 fused: f_out = F^{n+1} from f_in = F^n, then n += 1.  f_out != f_in.  One launch (plus a
- * solid-cell copy when the grid has solids) with the default scheme; see fks_set_scheme. */
+/* a1..a9 fused: f_out = F^{n+1} from f_in = F^n, then n += 1 (f_out == f_in: in place, see
+ * fks_collide).  One launch (plus a solid-cell copy when the grid has solids) with the default
+ * scheme; see fks_set_scheme. */
 fks_status fks_step(fks_ctx* ctx, const double* f_in, double* f_out, double dt);
 
 /* fks_step with HOST buffers: copies f_in_host to the device, steps, copies the result back
@@ -195,7 +199,7 @@ fks_status fks_step_host(fks_ctx* ctx, const double* f_in_host, double* f_out_ho
  * (the Maxwellian of the cell's moments projected onto them, so mass, momentum and
  * energy are exact).  nu_rule: FKS_NU_RHO (nu = rho), FKS_NU_CONST (nu = mu > 0),
  * FKS_NU_EULER (the tau -> 0 limit, F = E[f*]).  tau from fks_set_params.  Advances the step
- * counter like fks_step; solid cells are copied.  Device pointers, f_out != f_in. */
+ * counter like fks_step; solid cells are copied.  Device pointers (f_out == f_in: in place). */
 enum { FKS_NU_RHO = 0, FKS_NU_CONST = 1, FKS_NU_EULER = 2 };
 fks_status fks_step_bgk(fks_ctx* ctx, const double* f_in, double* f_out, double dt, int nu_rule, double mu);
 

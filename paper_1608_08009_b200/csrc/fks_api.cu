@@ -342,6 +342,7 @@ struct fks_ctx {
   int split = FKS_SPLIT_LIE;       // NEXT-4 time scheme (fks_set_scheme)
   int integ = FKS_TIME_EULER;
   double* d_tmp = nullptr;         // one state-sized scratch for the Heun / Strang sequences
+  double* d_inplace = nullptr;     // in-place calls (f_out == f_in): the result lands here first
   double* d_host_in = nullptr;
   double* d_host_out = nullptr;
   // fks_step_host pipeline (0D, no solids): copy streams and per-chunk events
@@ -1066,13 +1067,37 @@ fks_status fks_set_stream(fks_ctx* c, void* s) {
   return FKS_OK;
 }
 
-fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
-  if (!c || !f || !Q || f == Q) return FKS_E_INVAL;
+// §8(b) in-place calls: with f_out == f_in the call writes a library-owned state-sized buffer
+// (allocated on first use), then one device-to-device copy on the context stream moves it back.
+static fks_status ensure_inplace(fks_ctx* c) {
+  if (c->d_inplace) return FKS_OK;
+  return cudaMalloc(&c->d_inplace, (size_t)c->ncells * c->n * sizeof(double)) == cudaSuccess ? FKS_OK
+                                                                                                  : FKS_E_NOMEM;
+}
+
+extern "C++" {
+template <typename Call>
+static fks_status maybe_inplace(fks_ctx* c, const double* in, double* out, Call&& call) {
+  if (in != out) return call(out);
+  fks_status st = ensure_inplace(c);
+  if (st != FKS_OK) return st;
+  if ((st = call(c->d_inplace)) != FKS_OK) return st;
+  return cuda_fail(cudaMemcpyAsync(out, c->d_inplace, (size_t)c->ncells * c->n * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+}
+}
+
+static fks_status collide_impl(fks_ctx* c, const double* f, double* Q) {
   fks::StepParams p = base_params(c, f, Q, 0);
   fill_transport(c, &p.tp, false);  // no shifts: cannot fail
   p.cell_list = nullptr;
   p.ncells = (int)c->ncells;
   return run_collision(c, p);
+}
+
+fks_status fks_collide(fks_ctx* c, const double* f, double* Q) {
+  if (!c || !f || !Q) return FKS_E_INVAL;
+  return maybe_inplace(c, f, Q, [&](double* out) { return collide_impl(c, f, out); });
 }
 
 static fks_status check_dt(fks_ctx* c, double dt) {
@@ -1091,8 +1116,7 @@ static fks_status check_dt(fks_ctx* c, double dt) {
   return FKS_OK;
 }
 
-fks_status fks_transport(fks_ctx* c, const double* f_in, double* f_out, double dt) {
-  if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
+static fks_status transport_impl(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
   fks::TransportParams tp;
@@ -1174,8 +1198,7 @@ static fks_status step_scheme(fks_ctx* c, const double* f_in, double* f_out) {
   return transport_pass(c, tmp, f_out, h2);
 }
 
-fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
-  if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
+static fks_status step_impl(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
   if (c->integ != FKS_TIME_EULER || (c->split == FKS_SPLIT_STRANG && c->grid.dx > 0)) {
@@ -1214,8 +1237,7 @@ fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
   return FKS_OK;
 }
 
-fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt, int nu_rule, double mu) {
-  if (!c || !f_in || !f_out || f_in == f_out) return FKS_E_INVAL;
+static fks_status step_bgk_impl(fks_ctx* c, const double* f_in, double* f_out, double dt, int nu_rule, double mu) {
   if (nu_rule < FKS_NU_RHO || nu_rule > FKS_NU_EULER || (nu_rule == FKS_NU_CONST && !(mu > 0))) return FKS_E_INVAL;
   if (c->integ != FKS_TIME_EULER) return FKS_E_UNSUPPORTED;  // the BGK step is forward Euler only
   fks_status st = check_dt(c, dt);
@@ -1253,6 +1275,21 @@ fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt
   if (strang && (st = transport_pass(c, out1, f_out, h2)) != FKS_OK) return st;
   c->step_n++;
   return FKS_OK;
+}
+
+fks_status fks_transport(fks_ctx* c, const double* f_in, double* f_out, double dt) {
+  if (!c || !f_in || !f_out) return FKS_E_INVAL;
+  return maybe_inplace(c, f_in, f_out, [&](double* out) { return transport_impl(c, f_in, out, dt); });
+}
+
+fks_status fks_step(fks_ctx* c, const double* f_in, double* f_out, double dt) {
+  if (!c || !f_in || !f_out) return FKS_E_INVAL;
+  return maybe_inplace(c, f_in, f_out, [&](double* out) { return step_impl(c, f_in, out, dt); });
+}
+
+fks_status fks_step_bgk(fks_ctx* c, const double* f_in, double* f_out, double dt, int nu_rule, double mu) {
+  if (!c || !f_in || !f_out) return FKS_E_INVAL;
+  return maybe_inplace(c, f_in, f_out, [&](double* out) { return step_bgk_impl(c, f_in, out, dt, nu_rule, mu); });
 }
 
 // fks_step_host for independent cells (dx = 0, no solids): the batch is cut into chunks and
@@ -1495,6 +1532,7 @@ fks_status fks_finalize(fks_ctx* c) {
   cudaFree(c->d_host_in);
   cudaFree(c->d_host_out);
   cudaFree(c->d_tmp);
+  cudaFree(c->d_inplace);
   if (c->nccl) {
     if (c->s_comm) cudaStreamSynchronize(c->s_comm);  // no exchange in flight when the comm goes
     if (const NcclApi* nc = nccl_api()) nc->commDestroy(c->nccl);

@@ -459,9 +459,6 @@ def test_next_entry_points_argument_errors(torch, fks):
         with pytest.raises(fks.FksError) as ei:
             ctx.step_bgk(dev(torch, f), out, 0.01, rule, mu)
         assert ei.value.status == -1  # FKS_E_INVAL
-    a = dev(torch, f)
-    with pytest.raises(fks.FksError):
-        ctx.step_bgk(a, a, 0.01, bgk.NU_RHO, 0.0)  # in place is not allowed
     # specular reflection on a partitioned grid needs the library exchange (the neighbours' solid
     # flags): with caller-owned halo planes the step is refused
     ctx2 = fks.Context(3, 1, [4], N, L, 24, h=0.1, bc=[fks.BC_HALO, fks.BC_OUTFLOW])
@@ -613,3 +610,43 @@ def test_full_size_spatial_sampled(torch, fks, name, sample):
         Q = oproj.project_zero_moments(collision.collide_fft(fstar[i], tab), dv, N, L)
         ref = fstar[i] + (c["dt"] / c["tau"]) * Q
         assert np.max(np.abs(got[cell] - ref)) <= TOL * np.max(np.abs(ref)), (name, cell)
+
+
+@pytest.mark.parametrize("scheme", [None, "heun_strang"])
+def test_in_place_calls_bitwise(torch, fks, scheme):
+    """§8(b) in-place calls (f_out == f_in: the north_star's fks_step(f, dt)): collide, transport,
+    step and step_bgk on one buffer equal the out-of-place calls bitwise (1D x 3D, ghost / outflow
+    faces, a solid cell; the default scheme and Heun + Strang)."""
+    N, L, M = 8, 7.0, [6]
+    bc = [transport.GHOST, transport.OUTFLOW]
+    h = 0.1
+    dt = 0.9 * h / (L - L / N)
+    F = workloads.family("smooth", 3, N, L, 6, seed=17) * np.linspace(0.6, 1.4, 6)[:, None, None, None]
+    g = workloads.family("smooth", 3, N, L, 1, seed=18)[0]
+    solid = np.array([0, 0, 1, 0, 0, 0], dtype=bool)
+    ctxs = []
+    for _ in range(2):
+        c = fks.Context(3, 1, M, N, L, 24, h=h, bc=bc)
+        c.set_ghost(0, dev(torch, g))
+        c.set_solid(solid)
+        if scheme:
+            c.set_scheme(fks.SPLIT_STRANG, fks.TIME_HEUN)
+        ctxs.append(c)
+    a = dev(torch, F)
+    b = torch.empty_like(a)
+    ctxs[0].collide(a, b)
+    x = a.clone()
+    ctxs[1].collide(x, x)
+    assert torch.equal(x, b)
+    calls = [lambda c, i, o: c.step(i, o, dt), lambda c, i, o: c.transport(i, o, dt)]
+    if not scheme:
+        calls.append(lambda c, i, o: c.step_bgk(i, o, dt, bgk.NU_RHO, 0.0))
+    x = a.clone()
+    for call in calls:
+        b = torch.empty_like(a)
+        call(ctxs[0], a, b)
+        call(ctxs[1], x, x)
+        assert torch.equal(x, b)
+        a = b
+    for c in ctxs:
+        c.check()
