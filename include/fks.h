@@ -68,8 +68,8 @@ typedef struct {
 
 /* Create a context (P:85-91 model; P:141-158 kernels).
  *   grid          physical grid (copied).
- *   Nv            points per velocity axis: 8, 16, 32 or 64 (the paper uses 8..64 per axis,
- *                 P:624-625); else FKS_E_INVAL.
+ *   Nv            points per velocity axis: 4, 8, 16, 32 or 64 (4 <= N <= 64, S:28;
+ *                 the paper uses 8..64 per axis); else FKS_E_INVAL.
  *   L             velocity box half-width (> 0).
  *   M_dirs        number of quadrature directions A: dv = 2 -> theta_p = pi p / A, p = 1..A
  *                 (P:490); dv = 3 -> 24 = the spherical 7-design (reading #17), a perfect

@@ -15,7 +15,7 @@ _TAG = "checked" if CHECKED else "timing" if TIMING else os.environ.get("FKS_VAR
 LIB = os.path.join(HERE, f"libfks_{_TAG}.so" if _TAG else "libfks.so")
 OBJDIR = os.path.join(CSRC, _TAG) if _TAG else CSRC
 SOURCES = ["fks_api.cu", "kernels2d.cu", "kernels2dp.cu", "kernels3d.cu", "kernels3d64.cu", "kernels_aux.cu",
-           "kernels_bgk.cu"]
+           "kernels_bgk.cu", "kernels_small.cu"]
 HEADERS = ["fft.cuh", "fftp.cuh", "common.cuh", "kernels.cuh", os.path.join("..", "..", "include", "fks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + (["-DFKS_CHECKS"] if CHECKED else []) + os.environ.get("FKS_NVCC_EXTRA", "").split() + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

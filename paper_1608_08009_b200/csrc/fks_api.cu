@@ -401,7 +401,7 @@ fks_status upload_tables(fks_ctx* c) {
                  : make_double2(s * D[k] / n, 0.0);
   };
   std::vector<double2> T;
-  if (c->dv == 2 || N == 64) {  // T[p][k], k = l_x + N l_y (+ N^2 l_z)
+  if (c->dv == 2 || N == 64 || N == 4) {  // T[p][k], k = l_x + N l_y (+ N^2 l_z)
     T.resize((size_t)(A + 1) * n);
     for (int p = 0; p <= A; ++p)
       for (int k = 0; k < n; ++k) T[(size_t)p * n + k] = folded(p, k);
@@ -580,7 +580,9 @@ fks::StepParams base_params(fks_ctx* c, const double* f_in, double* f_out, int m
 fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
   if (p.ncells == 0) return FKS_OK;
   cudaError_t e;
-  if (c->dv == 3 && c->N == 64) {
+  if (c->N == 4) {
+    e = fks::launch_step_small(c->N, c->dv, p, c->sm_count, c->stream);
+  } else if (c->dv == 3 && c->N == 64) {
     const int ncl = std::min<int64_t>(p.ncells, c->nclusters);
     e = cudaMemsetAsync(c->d_sync, 0, (size_t)ncl * fks::sync_bytes3d64(), c->stream);
     if (e == cudaSuccess) e = fks::launch_step3d64(p, ncl, c->stream);
@@ -599,9 +601,9 @@ fks_status run_collision(fks_ctx* c, fks::StepParams& p) {
   return cuda_fail(e);
 }
 
-// Velocity nodes per axis: 8, 16, 32, 64 in 2D and 3D (P:624-625 quotes 16-64 per axis; 3D N = 64
-// runs kernels3d64.cu, a 64-CTA group per cell).
-bool valid_N(int N, int dv) { (void)dv; return N == 8 || N == 16 || N == 32 || N == 64; }
+// Velocity nodes per axis: 4, 8, 16, 32, 64 in 2D and 3D (4 <= N <= 64; the paper
+// quotes 8-64 per axis; 3D N = 64 runs kernels3d64.cu, N = 4 kernels_small.cu).
+bool valid_N(int N, int dv) { (void)dv; return N == 4 || N == 8 || N == 16 || N == 32 || N == 64; }
 
 }  // namespace
 
@@ -920,7 +922,9 @@ fks_status fks_init(const fks_grid* grid, int Nv, double L, int M_dirs, double k
     if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess) st = FKS_E_NOMEM;
     else cudaMemset(c->d_flag, 0, sizeof(int));
   }
-  if (st == FKS_OK && dv == 3) {
+  if (st == FKS_OK && Nv == 4) {
+    c->nclusters = c->sm_count * 8;  // kernels_small.cu: no groups; the round size of fks_step_host
+  } else if (st == FKS_OK && dv == 3) {
     c->nclusters = Nv == 64 ? fks::max_groups3d64() : fks::max_active_clusters3d(Nv);
     if (const char* e = getenv("FKS_MAX_CLUSTERS")) {  // development: scaling with the cluster count
       const int m = atoi(e);
@@ -1300,7 +1304,7 @@ static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, doubl
   fks_status st = check_dt(c, dt);
   if (st != FKS_OK) return st;
   const int64_t n = c->n;
-  const int64_t per_round = c->dv == 3 ? (int64_t)std::max(1, c->nclusters)
+  const int64_t per_round = (c->dv == 3 || c->N == 4) ? (int64_t)std::max(1, c->nclusters)
                                        : (int64_t)c->sm_count * (fks::use_pair2d(c->N, c->A) ? fks::cells_per_block2d_pair(c->N)
                                                                                           : fks::cells_per_block2d(c->N));
   int64_t nchunks = 32;  // FKS_HOST_CHUNKS: pipeline depth (C2: 12 chunks 25.6 ms, 32: 24.6 ms; PCIe-bound)

@@ -24,6 +24,9 @@ int max_groups3d64();
 size_t scratch_elems3d64();
 size_t sync_bytes3d64();
 
+// N = 4 (kernels_small.cu), 2D and 3D: one thread per velocity point, transforms in SMEM.
+cudaError_t launch_step_small(int N, int dv, const StepParams& p, int sm_count, cudaStream_t s);
+
 // 2D with pencils split over lane pairs (kernels2dp.cu): N = 64 (2 cells per 256-thread CTA) and
 // N = 32 (8 cells per 512-thread CTA, tables in SMEM when (A + 1) directions fit).
 cudaError_t launch_step2d_pair(int N, const StepParams& p, int nblocks, cudaStream_t s);

@@ -264,7 +264,7 @@ cudaError_t launch_moments(const double* f, double* rho, double* u, double* T, i
   }
 #define FKS_MO(NN, DD) \
   if (N == NN && dv == DD) { k_moments<NN, DD><<<nb, 256, 0, s>>>(f, rho, u, T, ncells, L, h); return cudaGetLastError(); }
-  FKS_MO(8, 2) FKS_MO(16, 2) FKS_MO(32, 2) FKS_MO(8, 3) FKS_MO(16, 3) FKS_MO(32, 3) FKS_MO(64, 3)
+  FKS_MO(4, 2) FKS_MO(8, 2) FKS_MO(16, 2) FKS_MO(32, 2) FKS_MO(4, 3) FKS_MO(8, 3) FKS_MO(16, 3) FKS_MO(32, 3) FKS_MO(64, 3)
 #undef FKS_MO
   return cudaErrorInvalidValue;
 }

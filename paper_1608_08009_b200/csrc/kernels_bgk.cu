@@ -536,7 +536,7 @@ cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStre
     else k_bgk<NN, DD, 256, 1><<<nb, 256, 0, s>>>(p, pf);                                    \
     return cudaGetLastError();                                                               \
   }
-  FKS_BGK(8, 2) FKS_BGK(16, 2) FKS_BGK(32, 2) FKS_BGK(64, 2) FKS_BGK(8, 3) FKS_BGK(16, 3) FKS_BGK(32, 3) FKS_BGK(64, 3)
+  FKS_BGK(4, 2) FKS_BGK(8, 2) FKS_BGK(16, 2) FKS_BGK(32, 2) FKS_BGK(64, 2) FKS_BGK(4, 3) FKS_BGK(8, 3) FKS_BGK(16, 3) FKS_BGK(32, 3) FKS_BGK(64, 3)
 #undef FKS_BGK
   return cudaErrorInvalidValue;
 }

@@ -41,7 +41,8 @@ def test_strerror(fks):
                                             (3, 8, 7.0, 24, None), (3, 16, 7.0, 24, None), (3, 8, 7.0, 64, None),
                                             (3, 16, 7.0, 24, 0.0), (3, 8, 7.0, 24, 0.5), (3, 16, 7.0, 64, 2.0),
                                             (3, 8, 7.0, 24, -0.5), (2, 32, 9.0, 8, 1.0), (2, 16, 6.0, 8, 0.3),
-                                            (2, 64, 12.0, 8, None), (3, 64, 7.0, 24, None)])
+                                            (2, 64, 12.0, 8, None), (3, 64, 7.0, 24, None),
+                                            (2, 4, 3.0, 8, None), (3, 4, 4.0, 24, None)])
 def test_host_tables_match_oracle(fks, dv, N, L, A, gamma):
     """Two independent table builders (C++ in the library, numpy in the oracle) agree to a few
     ulp: phi/psi (P:475, P:524, reading #2), directions (P:490, reading #17, reading #6),
@@ -117,8 +118,9 @@ def test_init_argument_validation(fks):
     (dict(dv=2, dx=3), -1),                             # dx <= dv (axis a shifts with velocity component a)
     (dict(dx=4), -1),
     (dict(dx=-1), -1),
-    (dict(Nv=24), -1),                                  # not in {8, 16, 32, 64}
-    (dict(Nv=4), -1),                                   # N = 4 is out of the supported range
+    (dict(Nv=24), -1),                                  # not a power of two in [4, 64]
+    (dict(Nv=2), -1),                                   # below the range 4 <= N <= 64
+    (dict(Nv=128), -1),                                 # above it
     (dict(L=0.0), -1),
     (dict(L=-3.0), -1),
     (dict(dx=1, M=[0]), -1),                            # empty axis
