@@ -82,7 +82,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-spatial-secondary", action="store_true", help="skip the C4 fused-step secondary figure")
+    ap.add_argument("--no-spatial-secondary", action="store_true", help="skip the C4 fused-step and 64^3 secondary figures")
     return ap.parse_args()
 
 
@@ -175,6 +175,39 @@ def oracle_rate(name, seconds=15.0, cores=None):
                                            "fft") for i in range(cores)])
     wall = max(times)  # workers run concurrently; each times only its own step loop
     return tot / wall, cores, tot, wall
+
+
+def n64_secondary(L, A, tau, dt, stream, reps, ncells=128):
+    """The 64^3 velocity grid (k_step3d64: a 64-CTA group per cell), not a BASELINE config: the
+    fused step on 128 homogeneous cells of the default workload's velocity box, CUDA events."""
+    import torch
+    import workloads
+    from paper_1608_08009_b200 import fks
+    N = 64
+    n = N ** 3
+    f = workloads.family("smooth", 3, N, L, 8, seed=5)
+    fa = torch.from_numpy(f).cuda().repeat(ncells // 8, 1, 1, 1).contiguous()
+    fb = torch.empty_like(fa)
+    ctx = fks.Context(3, 0, [ncells], N, L, A)
+    ctx.set_params(tau=tau)
+    ctx.set_stream(stream)
+    ctx.step(fa, fb, dt)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        ctx.step(fa, fb, dt)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ctx.check()
+    ctx.close()
+    del fa, fb
+    torch.cuda.empty_cache()
+    ach = flops_per_cell(3, N, A) * ncells / (ms * 1e-3) / 1e12
+    return {"value": ncells / (ms * 1e-3), "unit": "cells/s", "ms": ms, "fp64_frac": ach / FP64_PEAK_TFLOPS,
+            "phase_space_updates_per_s": ncells * n / (ms * 1e-3),
+            "what": f"fks_step on {ncells} homogeneous cells of a 64^3 velocity grid (k_step3d64), A = {A}"}
 
 
 def spatial_secondary(name, stream, reps):
@@ -439,6 +472,7 @@ def main():
         ctx.check()
         if c["dx_dim"] == 0 and dv == 3 and not a.no_spatial_secondary:
             extra["C4_fused_step"] = spatial_secondary("C4", stream, reps)
+            extra["N64_step"] = n64_secondary(c["L"], A, c["tau"], dt, stream, reps)
 
     # ---- e2e through the C ABI with host buffers (H2D + step + D2H per step) --------------
     e2e = None
