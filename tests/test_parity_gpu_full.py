@@ -295,8 +295,10 @@ def test_configuration_and_state_errors(torch, fks):
         (lambda: lib.fks_set_dirs(hnd, None, None, 0), -1),
         (lambda: lib.fks_set_state(hnd, -1, dt), -1),
         (lambda: lib.fks_moments(hnd, ctypes.c_void_p(f.data_ptr()), None, None, None), -1),
-        (lambda: lib.fks_step(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(f.data_ptr()), ctypes.c_double(dt)), -1),
-        (lambda: lib.fks_transport(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(f.data_ptr()), ctypes.c_double(dt)), -1),
+        (lambda: lib.fks_step(hnd, None, ctypes.c_void_p(o.data_ptr()), ctypes.c_double(dt)), -1),
+        (lambda: lib.fks_transport(hnd, ctypes.c_void_p(f.data_ptr()), None, ctypes.c_double(dt)), -1),
+        # in place is allowed; here it still fails on the unset ghost face, launching nothing
+        (lambda: lib.fks_step(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(f.data_ptr()), ctypes.c_double(dt)), -7),
         (lambda: lib.fks_step(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(o.data_ptr()), ctypes.c_double(0.0)), -1),
         (lambda: lib.fks_step(hnd, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(o.data_ptr()), ctypes.c_double(dt)), -7),  # ghost face 0 never set
     ):
