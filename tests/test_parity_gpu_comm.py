@@ -93,6 +93,8 @@ P, G_, O = transport.PERIODIC, transport.GHOST, transport.OUTFLOW
     (3, 3, [3, 2, 5], 8, [O, O, P, P, G_, O], 2, 7),
     (3, 3, [3, 3, 8], 8, [G_, O, O, O, P, P], 4, 20),    # ring of 4 along z
     (1, 3, [5], 64, [G_, O], 2, 2),                       # 64^3 (k_step3d64)
+    (2, 3, [4, 6], 4, [G_, O, P, P], 3, 5),               # N = 4 (k_step_small), periodic ring of 3
+    (2, 2, [5, 4], 4, [O, O, G_, O], 2, 7),
 ])
 def test_loopback_step_bitwise(torch, fks, dxd, dv, M, N, bc, world, solid_at):
     L = 6.0
@@ -182,6 +184,7 @@ def test_comm_argument_errors(torch, fks):
     (2, 3, [5, 8], 8, [G_, O, O, O], 2, [(2, 3), (2, 4), (3, 4), (1, 0), (4, 7)]),
     (2, 2, [6, 9], 16, [P, P, P, P], 3, [(2, 2), (3, 3), (2, 5), (4, 6), (0, 8), (5, 0)]),
     (3, 3, [4, 3, 6], 8, [O, O, P, P, P, P], 3, [(1, 1, 1), (1, 1, 2), (2, 2, 3), (0, 0, 5), (3, 2, 0)]),
+    (2, 3, [5, 6], 4, [G_, O, P, P], 2, [(2, 2), (2, 3), (1, 5), (3, 0)]),
 ])
 def test_loopback_specular_bitwise(torch, fks, dxd, dv, M, N, bc, world, solid_cells):
     """NEXT-1 on a partitioned grid: specular walls that straddle slab faces reflect exactly as in
@@ -217,7 +220,8 @@ def test_loopback_specular_C4_full_size(torch, fks):
 
 
 @pytest.mark.parametrize("dxd,dv,M,N,specular", [(1, 3, [6], 8, False), (2, 2, [4, 5], 16, False),
-                                                 (3, 3, [3, 2, 4], 8, True)])
+                                                 (3, 3, [3, 2, 4], 8, True), (2, 3, [3, 4], 4, True),
+                                                 (1, 3, [3], 64, False)])
 def test_nccl_single_rank_ring_bitwise(torch, fks, dxd, dv, M, N, specular):
     """The real NCCL path on one GPU: a one-rank communicator (fks_comm_unique_id + fks_set_comm,
     nranks = 1) whose slab axis is a periodic ring of one -- both HALO neighbours are the rank
