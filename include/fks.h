@@ -104,6 +104,24 @@ fks_status fks_set_ghost(fks_ctx* ctx, int face, const double* ghost_f);
  * fks_step / fks_transport calls (not copied); NULL for a face without a HALO. */
 fks_status fks_set_halo(fks_ctx* ctx, const double* lo_plane, const double* hi_plane);
 
+/* a2 fused into the step over peer memory: a rank maps its neighbours' state buffers (CUDA IPC;
+ * NVLink / NVSwitch peers of one box, or another process on the same GPU) and hands fks_set_halo
+ * pointers to THEIR boundary planes -- the lower neighbour's last plane, the upper one's first --
+ * so the step's transport gather reads the sources across the slab face straight from the peer:
+ * no pack, send, receive or unpack (paper_1608_08009_b200.parallel.PeerHalo).  The
+ * caller orders the ranks' steps (a stream-ordered barrier per step: a rank's step n + 1 reads the
+ * neighbours' step-n output, and their step n + 2 overwrites the buffer it read).  Specular walls
+ * across the face need the neighbours' solid flags: library exchange only (fks_set_comm).
+ *   fks_ipc_get_handle: handle_out (FKS_IPC_HANDLE_BYTES bytes) of the device allocation that
+ *                       contains dptr, and the byte offset of dptr inside it;
+ *   fks_ipc_open:       maps a handle from another process; *base_out = the allocation base
+ *                       (add the owner's offset); FKS_E_CUDA if the peer cannot be mapped;
+ *   fks_ipc_close:      unmaps it. */
+#define FKS_IPC_HANDLE_BYTES 64
+fks_status fks_ipc_get_handle(const void* dptr, void* handle_out, int64_t* offset_out);
+fks_status fks_ipc_open(const void* handle, void** base_out);
+fks_status fks_ipc_close(void* base);
+
 /* a2 inside the library: the slab halo exchange of the paper's MPI z-slab decomposition
  * (Fig. mpi-decomp; ghost cells exchanged every step) over NCCL (NVLink /
  * NVSwitch between the GPUs of a box), one rank per GPU.  The slab axis is the slowest space axis

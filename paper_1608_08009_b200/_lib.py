@@ -33,6 +33,9 @@ SIGNATURES = {
     "fks_set_specular": (c_int, [c_void_p, c_int]),
     "fks_set_scheme": (c_int, [c_void_p, c_int, c_int]),
     "fks_comm_unique_id": (c_int, [c_void_p]),
+    "fks_ipc_get_handle": (c_int, [c_void_p, c_void_p, ctypes.POINTER(c_int64)]),
+    "fks_ipc_open": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "fks_ipc_close": (c_int, [c_void_p]),
     "fks_set_comm": (c_int, [c_void_p, c_void_p, c_int, c_int]),
     "fks_comm_loopback_create": (c_int, [c_int, ctypes.POINTER(c_void_p)]),
     "fks_comm_loopback_destroy": (c_int, [c_void_p]),

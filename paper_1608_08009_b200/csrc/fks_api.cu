@@ -1001,6 +1001,41 @@ fks_status fks_set_scheme(fks_ctx* c, int splitting, int integrator) {
   return FKS_OK;
 }
 
+// ---- peer memory (a2 fused into the gather) ----------------------------------
+fks_status fks_ipc_get_handle(const void* dptr, void* handle_out, int64_t* offset_out) {
+  if (!dptr || !handle_out || !offset_out) return FKS_E_INVAL;
+  // the allocation containing dptr (a caching allocator hands out interior pointers): driver API,
+  // dlopen'ed like NCCL so that libfks links the runtime only
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static const GetRange get_range = []() -> GetRange {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    return h ? reinterpret_cast<GetRange>(dlsym(h, "cuMemGetAddressRange_v2")) : nullptr;
+  }();
+  if (!get_range) return FKS_E_CUDA;
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dptr)) != 0) return FKS_E_INVAL;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) return FKS_E_CUDA;
+  static_assert(sizeof(h) == FKS_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)(reinterpret_cast<unsigned long long>(dptr) - base);
+  return FKS_OK;
+}
+
+fks_status fks_ipc_open(const void* handle, void** base_out) {
+  if (!handle || !base_out) return FKS_E_INVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cuda_fail(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+fks_status fks_ipc_close(void* base) {
+  if (!base) return FKS_E_INVAL;
+  return cuda_fail(cudaIpcCloseMemHandle(base));
+}
+
 fks_status fks_comm_unique_id(void* id_out) {
   if (!id_out) return FKS_E_INVAL;
   const NcclApi* nc = nccl_api();

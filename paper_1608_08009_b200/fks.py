@@ -77,6 +77,13 @@ class Context:
                                      _ptr(hi) if hi is not None else None), "fks_set_halo")
         self._halo_refs = (lo, hi)  # keep the buffers alive while the library holds the pointers
 
+    def set_halo_ptr(self, lo, hi):
+        """fks_set_halo with raw device addresses (ints, or None): e.g. a peer's boundary plane
+        mapped with ipc_open (parallel.PeerHalo).  The caller keeps the memory alive."""
+        check(self._lib.fks_set_halo(self.handle, ctypes.c_void_p(lo) if lo is not None else None,
+                                     ctypes.c_void_p(hi) if hi is not None else None), "fks_set_halo")
+        self._halo_refs = None
+
     def set_solid(self, mask):
         if mask is None:
             check(self._lib.fks_set_solid(self.handle, None), "fks_set_solid")
@@ -181,6 +188,26 @@ def comm_unique_id():
     buf = ctypes.create_string_buffer(128)
     check(load().fks_comm_unique_id(buf), "fks_comm_unique_id")
     return buf.raw
+
+
+def ipc_handle(tensor):
+    """fks_ipc_get_handle: (64-byte handle, byte offset) of the allocation holding a CUDA tensor."""
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    check(load().fks_ipc_get_handle(ctypes.c_void_p(tensor.data_ptr()), buf, ctypes.byref(off)),
+          "fks_ipc_get_handle")
+    return buf.raw, off.value
+
+
+def ipc_open(handle):
+    """fks_ipc_open: map another process's allocation; returns its base address (int)."""
+    base = ctypes.c_void_p()
+    check(load().fks_ipc_open(ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(base)), "fks_ipc_open")
+    return base.value
+
+
+def ipc_close(base):
+    check(load().fks_ipc_close(ctypes.c_void_p(base)), "fks_ipc_close")
 
 
 # ---- function-style aliases with the C names ---------------------------------------------

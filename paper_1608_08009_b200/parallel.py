@@ -174,3 +174,76 @@ class DistributedStep:
         lo, hi = self.x.exchange(f_in)
         self.ctx.set_halo(lo, hi)
         self.ctx.step(f_in, f_out, dt)
+
+
+def peer_plane_addresses(slab, n, lower_bases, lower_cells, upper_bases, itemsize=8):
+    """Byte addresses of the neighbour planes a rank's HALO faces read, per buffer parity:
+    lo[b] = the lower neighbour's LAST plane of its buffer b (its local cells `lower_cells`),
+    hi[b] = the upper neighbour's FIRST plane.  None where the slab face is a domain face."""
+    plane = slab.plane_cells * n * itemsize
+    lo = [None, None] if lower_bases is None else [b + lower_cells * n * itemsize - plane for b in lower_bases]
+    hi = [None, None] if upper_bases is None else list(upper_bases)
+    return lo, hi
+
+
+class PeerHalo:
+    """a2 fused into the step over peer memory (include/fks.h fks_ipc_*).
+
+    Every rank keeps its state in two ping-pong buffers; once, the ranks exchange CUDA IPC handles
+    of them (torch.distributed.all_gather_object) and map their neighbours' buffers.  Each step
+    then points fks_set_halo at the neighbours' boundary planes of the current parity, so the step
+    kernel's transport gather reads the sources across a slab face straight from the peer GPU
+    (NVLink / NVSwitch): no pack, send, receive or unpack kernels, no staging copy.  Ordering is
+    one barrier per step (`barrier`, default a 1-element all_reduce on the current stream, which
+    NCCL orders with the kernels): step n + 1 reads the neighbours' step-n output, and their step
+    n + 2 overwrites that buffer only after everyone passed the next barrier.  Specular walls across
+    a face need the neighbours' solid flags: use init_libfks_comm for those runs."""
+
+    def __init__(self, ctx, slab, bufs, group=None, barrier=None):
+        import torch
+        import torch.distributed as dist
+        from . import fks
+        self.ctx, self.slab, self.bufs = ctx, slab, bufs
+        n = bufs[0][0].numel()
+        ncells = bufs[0].shape[0]
+        mine = ([fks.ipc_handle(b) for b in bufs], ncells)
+        every = [None] * slab.world
+        dist.all_gather_object(every, mine, group=group)
+        self._mapped = {}
+
+        def bases(q):
+            if q is None:
+                return None
+            if q == slab.rank:  # a periodic ring of one rank: its own buffers
+                return [b.data_ptr() for b in bufs]
+            if q not in self._mapped:
+                self._mapped[q] = [fks.ipc_open(h) for h, _ in every[q][0]]
+            return [base + off for base, (_, off) in zip(self._mapped[q], every[q][0])]
+
+        lo_q, hi_q = slab.lower(), slab.upper()
+        self.lo, self.hi = peer_plane_addresses(slab, n, bases(lo_q), every[lo_q][1] if lo_q is not None else 0,
+                                                bases(hi_q))
+        if barrier is None:
+            token = torch.zeros(1, device=bufs[0].device)
+
+            def barrier():
+                dist.all_reduce(token, group=group)
+        self.barrier = barrier
+        self.parity = 0
+        ctx.set_stream(torch.cuda.current_stream(bufs[0].device))
+
+    def step(self, dt):
+        """One fused step: bufs[parity] -> bufs[1 - parity]; returns the output buffer."""
+        self.barrier()
+        b = self.parity
+        self.ctx.set_halo_ptr(self.lo[b], self.hi[b])
+        self.ctx.step(self.bufs[b], self.bufs[1 - b], dt)
+        self.parity ^= 1
+        return self.bufs[1 - b]
+
+    def close(self):
+        from . import fks
+        for bases in self._mapped.values():
+            for b in bases:
+                fks.ipc_close(b)
+        self._mapped = {}

@@ -192,3 +192,34 @@ def test_libfks_halo_plan_gloo(case, world):
     out = ctx.Manager().dict()
     mp.start_processes(_worker_libplan, args=(world, _free_port(), case, out), nprocs=world, start_method="spawn")
     assert dict(out) == {r: True for r in range(world)}
+
+
+@pytest.mark.parametrize("world,periodic", [(3, False), (4, True), (1, True)])
+def test_peer_plane_addresses(world, periodic):
+    """PeerHalo's pointer arithmetic against the global layout: with the ranks' buffers laid out
+    back to back as one global array, the lower neighbour's last plane and the upper neighbour's
+    first plane are exactly the global planes next to the slab (halos_from_global)."""
+    M, n = [3, 2, 11], 5
+    bc = [BC_OUTFLOW] * 4 + ([BC_PERIODIC] * 2 if periodic else [BC_GHOST, BC_OUTFLOW])
+    slabs = [parallel.decompose(3, M, bc, world, r) for r in range(world)]
+    pc = slabs[0].plane_cells
+    # buffer b of rank r lives at base 10**6 * (2 r + b + 1) bytes; its planes are the slab's planes
+    base = {(r, b): 10 ** 6 * (2 * r + b + 1) for r in range(world) for b in range(2)}
+    for s in slabs:
+        lo_q, hi_q = s.lower(), s.upper()
+        lo, hi = parallel.peer_plane_addresses(
+            s, n, [base[(lo_q, b)] for b in range(2)] if lo_q is not None else None,
+            int(np.prod(slabs[lo_q].M_local)) if lo_q is not None else 0,
+            [base[(hi_q, b)] for b in range(2)] if hi_q is not None else None)
+        for b in range(2):
+            if lo_q is None:
+                assert lo[b] is None
+            else:
+                q = slabs[lo_q]
+                # the global plane just below s.lo is plane (hi - 1) of rank lo_q
+                assert s.lo - 1 == q.hi - 1 or (periodic and s.lo == 0 and q.hi == M[2])
+                assert lo[b] == base[(lo_q, b)] + ((q.hi - q.lo) - 1) * pc * n * 8
+            if hi_q is None:
+                assert hi[b] is None
+            else:
+                assert hi[b] == base[(hi_q, b)]
