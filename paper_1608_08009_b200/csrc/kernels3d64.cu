@@ -43,6 +43,10 @@ constexpr int T64 = 128;                 // threads per CTA: one lane pair per p
 constexpr int CTAS64 = FKS_N64_CTAS;     // resident CTAs per SM (2, or 3 with f* re-gathered)
 constexpr bool FS_TMEM64 = CTAS64 == 2;  // f* cached in TMEM for the loss term and the update
 constexpr int TMEM64 = FS_TMEM64 ? 256 : 128;  // f^ (32 complex = 128 columns) [+ f* (32 fp64 = 64 columns)]
+#ifndef FKS_N64_BATCH
+#define FKS_N64_BATCH 1
+#endif
+constexpr int NB64 = FKS_N64_BATCH;  // directions per group barrier
 
 // Group barrier counter and the projection partials of one group (zeroed before every launch).
 struct Sync64 {
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(T64, CTAS64) k_step3d64(const StepParams p) {
   const int t = threadIdx.x, q = t >> 1, h = t & 1, w = t >> 5;
   const int rank = blockIdx.x % P64, grp = blockIdx.x / P64, ngrp = gridDim.x / P64;
   Sync64* gs = reinterpret_cast<Sync64*>(p.sync) + grp;
-  double2* wbuf = p.scratch + (size_t)grp * 2 * n;  // two exchange buffers [j_z or l_z][l_y][l_x]
+  double2* wbuf = p.scratch + (size_t)grp * 2 * NB64 * n;  // exchange slots [j_z or l_z][l_y][l_x]
   load_delta(p.tp, sdelta);
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -196,13 +200,13 @@ __global__ void __launch_bounds__(T64, CTAS64) k_step3d64(const StepParams p) {
 #pragma unroll
       for (int j = 0; j < H; ++j) c[j] = pl[sw64(H * h + j, q)];
       fftp_dif<N, -1>(c, h);
-      double2* wb = wbuf + (size_t)(item & 1) * n + (size_t)rank * PL + q;
+      double2* wb = wbuf + (size_t)((item & 1) * NB64) * n + (size_t)rank * PL + q;
 #pragma unroll
       for (int m = 0; m < H; ++m) __stcg(wb + (2 * m + h) * N, c[m]);
     }
     group_bar(gs, target);
     {  // F2: pencil (l_x = q, l_y = rank), z halves, DIF along z -> f^ (l_z = 2m + h) in TMEM
-      const double2* wb = wbuf + (size_t)(item & 1) * n + (size_t)rank * N + q;
+      const double2* wb = wbuf + (size_t)((item & 1) * NB64) * n + (size_t)rank * N + q;
       double2 c[H];
 #pragma unroll
       for (int j = 0; j < H; ++j) c[j] = __ldcg(wb + (size_t)(H * h + j) * PL);
@@ -225,76 +229,89 @@ __global__ void __launch_bounds__(T64, CTAS64) k_step3d64(const StepParams p) {
     double gacc[H];  // G (then Q) at (x = H h + j, y = q, z = rank)
 #pragma unroll
     for (int j = 0; j < H; ++j) gacc[j] = 0.0;
-#pragma unroll 1
-    for (int d = 0; d <= p.A; ++d) {
-      double2* wb = wbuf + (size_t)(item & 1) * n;
-      {  // I1: X = T f^ on pencil (q, rank), DIT IFFT along z -> exchange [j_z = H h + j][rank][q]
-        // the next direction's table rows of this pencil plane -> L2 (read-only, one item ahead)
-        if (d < p.A && t < N)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.tables + (size_t)(d + 1) * n +
-                                                                            (size_t)t * PL + (size_t)rank * N),
-                       "r"((uint32_t)(N * sizeof(double2)))
-                       : "memory");
-        double2 c[H];
-        const double2* td = p.tables + (size_t)d * n + (size_t)rank * N + q;
+    // the directions in batches of NB64 per group barrier (exchange slots: batch parity x NB64)
+    auto pencils = [&](int d, int slot) {
+        {  // I1: X = T f^ on pencil (q, rank), DIT IFFT along z -> exchange [j_z = H h + j][rank][q]
+          // the next direction's table rows of this pencil plane -> L2 (read-only, one item ahead)
+          if (d < p.A && t < N)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.tables + (size_t)(d + 1) * n +
+                                                                              (size_t)t * PL + (size_t)rank * N),
+                         "r"((uint32_t)(N * sizeof(double2)))
+                         : "memory");
+          double2 c[H];
+          const double2* td = p.tables + (size_t)d * n + (size_t)rank * N + q;
 #pragma unroll
-        for (int m = 0; m < H; ++m) {  // all 32 table loads in flight (l_z = 2m + h)
-          FKS_CHECK((int64_t)d * n + (int64_t)(2 * m + h) * PL + rank * N + q < p.table_elems);
-          c[m] = __ldg(td + (size_t)(2 * m + h) * PL);
-        }
-#pragma unroll
-        for (int ch = 0; ch < H / 8; ++ch) {
-          uint32_t v[32];
-          tm_ld32(faddr + ch * 32, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
-            const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
-            const double2 tt = c[ch * 8 + i];
-            c[ch * 8 + i] = make_double2(fma(tt.x, Fx, -tt.y * Fy), fma(tt.x, Fy, tt.y * Fx));
+          for (int m = 0; m < H; ++m) {  // all 32 table loads in flight (l_z = 2m + h)
+            FKS_CHECK((int64_t)d * n + (int64_t)(2 * m + h) * PL + rank * N + q < p.table_elems);
+            c[m] = __ldg(td + (size_t)(2 * m + h) * PL);
           }
-        }
-        fftp_dit<N, +1>(c, h);
-        double2* o = wb + (size_t)rank * N + q;
 #pragma unroll
-        for (int j = 0; j < H; ++j) __stcg(o + (size_t)(H * h + j) * PL, c[j]);
-      }
-      group_bar(gs, target);
-      {  // I2: plane j_z = rank, column l_x = q, rows l_y = 2m + h, DIT IFFT along y -> SMEM
-        const double2* src = wb + (size_t)rank * PL + q;
-        double2 c[H];
-#pragma unroll
-        for (int m = 0; m < H; ++m) c[m] = __ldcg(src + (2 * m + h) * N);
-        fftp_dit<N, +1>(c, h);
-#pragma unroll
-        for (int j = 0; j < H; ++j) pl[sw64(H * h + j, q)] = c[j];
-      }
-      __syncthreads();
-      {  // I2: row j_y = q, columns l_x = 2m + h, DIT IFFT along x, accumulate
-        double2 r[H];
-#pragma unroll
-        for (int m = 0; m < H; ++m) r[m] = pl[sw64(q, 2 * m + h)];
-        fftp_dit<N, +1>(r, h);
-        if (d < p.A) {
-#pragma unroll
-          for (int j = 0; j < H; ++j) gacc[j] = fma(r[j].x, r[j].y, gacc[j]);
-        } else if constexpr (FS_TMEM64) {
-#pragma unroll
-          for (int ch = 0; ch < H / 16; ++ch) {
+          for (int ch = 0; ch < H / 8; ++ch) {
             uint32_t v[32];
-            tm_ld32(saddr + ch * 32, v);
+            tm_ld32(faddr + ch * 32, v);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const double fs = __hiloint2double(v[2 * i + 1], v[2 * i]);
-              gacc[ch * 16 + i] = gacc[ch * 16 + i] - fs * r[ch * 16 + i].x;  // Q = G - f* c
+            for (int i = 0; i < 8; ++i) {
+              const double Fx = __hiloint2double(v[4 * i + 1], v[4 * i + 0]);
+              const double Fy = __hiloint2double(v[4 * i + 3], v[4 * i + 2]);
+              const double2 tt = c[ch * 8 + i];
+              c[ch * 8 + i] = make_double2(fma(tt.x, Fx, -tt.y * Fy), fma(tt.x, Fy, tt.y * Fx));
             }
           }
-        } else {
+          fftp_dit<N, +1>(c, h);
+          double2* o = wbuf + (size_t)slot * n + (size_t)rank * N + q;
 #pragma unroll
-          for (int j = 0; j < H; ++j) gacc[j] = gacc[j] - fstar_at(j) * r[j].x;
+          for (int j = 0; j < H; ++j) __stcg(o + (size_t)(H * h + j) * PL, c[j]);
         }
+    };
+    auto planes = [&](int d, int slot) {
+        {  // I2: plane j_z = rank, column l_x = q, rows l_y = 2m + h, DIT IFFT along y -> SMEM
+          const double2* src = wbuf + (size_t)slot * n + (size_t)rank * PL + q;
+          double2 c[H];
+#pragma unroll
+          for (int m = 0; m < H; ++m) c[m] = __ldcg(src + (2 * m + h) * N);
+          fftp_dit<N, +1>(c, h);
+#pragma unroll
+          for (int j = 0; j < H; ++j) pl[sw64(H * h + j, q)] = c[j];
+        }
+        __syncthreads();
+        {  // I2: row j_y = q, columns l_x = 2m + h, DIT IFFT along x, accumulate
+          double2 r[H];
+#pragma unroll
+          for (int m = 0; m < H; ++m) r[m] = pl[sw64(q, 2 * m + h)];
+          fftp_dit<N, +1>(r, h);
+          if (d < p.A) {
+#pragma unroll
+            for (int j = 0; j < H; ++j) gacc[j] = fma(r[j].x, r[j].y, gacc[j]);
+          } else if constexpr (FS_TMEM64) {
+#pragma unroll
+            for (int ch = 0; ch < H / 16; ++ch) {
+              uint32_t v[32];
+              tm_ld32(saddr + ch * 32, v);
+              asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const double fs = __hiloint2double(v[2 * i + 1], v[2 * i]);
+                gacc[ch * 16 + i] = gacc[ch * 16 + i] - fs * r[ch * 16 + i].x;  // Q = G - f* c
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < H; ++j) gacc[j] = gacc[j] - fstar_at(j) * r[j].x;
+          }
+        }
+    };
+#pragma unroll 1
+    for (int d0 = 0; d0 <= p.A; d0 += NB64) {
+      const int nb = min(NB64, p.A + 1 - d0);
+      const int slot0 = (int)(item & 1) * NB64;
+#pragma unroll 1
+      for (int e = 0; e < nb; ++e) pencils(d0 + e, slot0 + e);
+      group_bar(gs, target);
+#pragma unroll 1
+      for (int e = 0; e < nb; ++e) {
+        if (e > 0) __syncthreads();  // the plane of the previous direction read
+        planes(d0 + e, slot0 + e);
       }
       ++item;
     }
@@ -417,7 +434,7 @@ int max_groups3d64() {
             fa.numRegs, SMEM64);
   return per_sm * sms / P64;
 }
-size_t scratch_elems3d64() { return (size_t)2 * NN64; }
+size_t scratch_elems3d64() { return (size_t)2 * NB64 * NN64; }
 
 size_t sync_bytes3d64() { return sizeof(Sync64); }
 
