@@ -4,22 +4,24 @@
 // z = IFFT((alpha~_p + i alpha'~_p) f^), G += Re z Im z (reading #10); the loss as the
 // (A+1)-th item with table (D~, 0), Q = G - f* Re z; projection; Euler
 // P:273-275 or the Heun stage), but one 64^3 complex field is 4 MiB, so a cell is owned by a group
-// of P64 = 64 co-resident CTAs (cooperative launch) and each transform goes through L2 twice:
+// of P64 = 64 co-resident CTAs (launch_step3d64) and each transform goes through L2 twice:
 //   CTA r owns the spectrum pencils (l_x, l_y = r, all l_z) -- f^ resident in its TMEM -- and the
 //   output plane j_z = r -- the gain accumulator G in registers, f* cached in TMEM.
 // Per direction: (I1) X = T f^ on the CTA's 64 pencils, IFFT along z, pencils written to the
 // group's exchange buffer; group barrier; (I2) the CTA's j_z plane read back, IFFT along y
 // (columns, registers -> SMEM), IFFT along x (rows, SMEM -> registers), accumulate.  The forward
 // transform (a4) runs the same passes in the other order: plane FFT along x then y (F1), barrier,
-// pencil FFT along z into TMEM (F2).  Two exchange buffers alternate, so one barrier per item
-// suffices: a CTA writing item t + 2 has passed barrier t + 1, which every CTA reaches only after
-// reading item t.  (Software-pipelining the next direction's pencils into the barrier wait, with
-// a ring of four buffers, measured slower: 10.45 vs 10.0 ms per 128-cell step.)
+// pencil FFT along z into TMEM (F2).  Two sets of exchange slots alternate (NB64 directions per
+// barrier, one set each), so one barrier per batch suffices: a CTA writing batch t + 2 has passed
+// barrier t + 1, which every CTA reaches only after reading batch t.  (Measured alternatives:
+// profiles/r02_n64.md -- software-pipelining the next direction's pencils into the barrier wait,
+// 2-4 directions per barrier, 3 CTAs per SM: all slower.)
 // Every 64-point pencil is split over a lane pair (fftp.cuh): 128 threads = 64 pencils, two CTAs
-// (two different groups) per SM, all CTAs co-resident (launch_step3d64).  Tables: full layout T[p][l_z][l_y][l_x], pre-folded as in
-// kernels3d.cu (alpha~ = s w_p alpha_p / n, alpha'~ = alpha'_p / n, D~ = s D / n).
-#include <cstdio>
+// (two different groups) per SM, all CTAs co-resident (launch_step3d64).  Tables: full layout
+// T[p][l_z][l_y][l_x], pre-folded as in kernels3d.cu (alpha~ = s w_p alpha_p / n,
+// alpha'~ = alpha'_p / n, D~ = s D / n).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -148,7 +150,7 @@ __global__ void __launch_bounds__(T64, CTAS64) k_step3d64(const StepParams p) {
   const uint32_t faddr = tbase + ((uint32_t)(32 * w) << 16);  // f^ of pencil (q, rank), l_z = 2m + h
   const uint32_t saddr = faddr + 128;                          // f*(x = H h + j, y = q, z = rank)
   unsigned target = 0;  // group barriers so far x P64
-  unsigned item = 0;    // exchange items so far (buffer item & 1)
+  unsigned item = 0;    // exchange batches so far (slot set item & 1)
 
   for (int it = grp; it < p.ncells; it += ngrp) {
     const int64_t cell = p.cell_list ? p.cell_list[it] : it;
