@@ -1342,8 +1342,11 @@ static fks_status step_host_pipelined(fks_ctx* c, const double* f_in_host, doubl
   const int64_t per_round = (c->dv == 3 || c->N == 4) ? (int64_t)std::max(1, c->nclusters)
                                        : (int64_t)c->sm_count * (fks::use_pair2d(c->N, c->A) ? fks::cells_per_block2d_pair(c->N)
                                                                                           : fks::cells_per_block2d(c->N));
-  int64_t nchunks = 32;  // FKS_HOST_CHUNKS: pipeline depth (C2: 12 chunks 25.6 ms, 32: 24.6 ms; PCIe-bound)
-  if (const char* e = getenv("FKS_HOST_CHUNKS")) nchunks = std::max(1, atoi(e));
+  // FKS_HOST_CHUNKS: pipeline depth (C2: 12 chunks 25.6 ms, 32: 24.6 ms; PCIe-bound), read once
+  static const int64_t nchunks = [] {
+    const char* e = getenv("FKS_HOST_CHUNKS");
+    return e ? (int64_t)std::max(1, atoi(e)) : (int64_t)32;
+  }();
   int64_t chunk = std::max<int64_t>(per_round * 2, (c->ncells + nchunks - 1) / nchunks);
   chunk = (chunk + per_round - 1) / per_round * per_round;  // whole rounds of the persistent grid
   const int nch = (int)((c->ncells + chunk - 1) / chunk);

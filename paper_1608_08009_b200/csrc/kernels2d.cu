@@ -368,8 +368,11 @@ int cells_per_block2d(int N) {
 bool use_pair2d(int N, int A) {
   if (N == 64) return true;
   if (N != 32 || !step2d_pair_fits(N, A)) return false;
-  const char* e = getenv("FKS_2D_PAIR");
-  return e && atoi(e) == 1;
+  static const bool knob = [] {  // development knob, read once
+    const char* e = getenv("FKS_2D_PAIR");
+    return e && atoi(e) == 1;
+  }();
+  return knob;
 }
 
 }  // namespace fks

@@ -497,8 +497,10 @@ cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStre
   if (dv == 2 && p.tp.dx == 0) {
     // FKS_BGK2_CFG (experiment knob): resident CTAs per SM the register cap aims at (1, 3 or 4);
     // 3 (80 registers) measured best at the C1 shape (profiles/r01_optimisation_log.md)
-    int minb = 3;
-    if (const char* e = getenv("FKS_BGK2_CFG")) minb = atoi(e);
+    static const int minb = [] {  // read once
+      const char* e = getenv("FKS_BGK2_CFG");
+      return e ? atoi(e) : 3;
+    }();
     const int per_sm = minb == 1 ? 8 : 2 * minb;
     const unsigned nw = (unsigned)((p.ncells + 7) / 8 < sm_count * per_sm ? (p.ncells + 7) / 8 : sm_count * per_sm);
 #define FKS_BGK2(NN)                                                        \
@@ -515,12 +517,18 @@ cudaError_t launch_bgk(int N, int dv, const BgkParams& p, int sm_count, cudaStre
   // the 126 MB L2, or pass 3 re-reads f from HBM.  FKS_BGK_CFG (experiment knob) = 0: 256 threads x
   // 8 CTAs/SM + prefetch (the round-1 launch); 2: 512 x 2, no prefetch; 3: 512 x 1 + prefetch;
   // 4: 512 x 2 capped at 64 registers (2 resident), no prefetch; 5: 256 x 4 at 64 registers.
-  int cfg = (dv == 3 && N == 32) ? 6 : 0;
-  if (const char* e = getenv("FKS_BGK_CFG")) cfg = atoi(e);
+  static const int cfg_env = [] {  // read once; -1: not set
+    const char* e = getenv("FKS_BGK_CFG");
+    return e ? atoi(e) : -1;
+  }();
+  int cfg = cfg_env >= 0 ? cfg_env : (dv == 3 && N == 32) ? 6 : 0;
   if (cfg == 6 && dv == 3 && N == 32) {  // f* in TMEM: one 512-thread CTA per SM (all TMEM columns)
     const unsigned nb6 = (unsigned)(p.ncells < sm_count ? p.ncells : sm_count);
-    const char* bw = getenv("FKS_BGK_BW");  // experiment knob: gathers in flight per thread
-    if (bw && atoi(bw) == 32) k_bgk_tmem32<32><<<nb6, 512, 0, s>>>(p);
+    static const bool bw32 = [] {  // experiment knob: gathers in flight per thread (read once)
+      const char* e = getenv("FKS_BGK_BW");
+      return e && atoi(e) == 32;
+    }();
+    if (bw32) k_bgk_tmem32<32><<<nb6, 512, 0, s>>>(p);
     else k_bgk_tmem32<16><<<nb6, 512, 0, s>>>(p);
     return cudaGetLastError();
   }
