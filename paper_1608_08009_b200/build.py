@@ -23,6 +23,13 @@ FLAGS = (["-DFKS_TIMING"] if os.environ.get("FKS_TIMING") else []) + (["-DFKS_CH
          "--expt-relaxed-constexpr"]
 
 
+# Per-file ptxas settings.  kernels3d.cu: --register-usage-level=6 (default 5) gives k_step3d a
+# different register allocation, 17.88 vs 18.29 ms per C2 step (levels 6-10 produce the same SASS;
+# profiles/r02_optimisation_log.md); applied to the other files it costs the 2D N = 64 kernel
+# 20 % and the transport / BGK kernels 2-3 %, so it is not global.
+FILE_FLAGS = {"kernels3d.cu": ["-Xptxas", "--register-usage-level=6"]}
+
+
 def _stale():
     if not os.path.exists(LIB):
         return True
@@ -35,7 +42,7 @@ def _compile(s, verbose):
     src = os.path.join(CSRC, s)
     os.makedirs(OBJDIR, exist_ok=True)
     obj = os.path.join(OBJDIR, s.replace(".cu", ".o"))
-    r = subprocess.run([NVCC, *FLAGS, "-c", src, "-o", obj], capture_output=True, text=True)
+    r = subprocess.run([NVCC, *FLAGS, *FILE_FLAGS.get(s, []), "-c", src, "-o", obj], capture_output=True, text=True)
     if verbose or r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
     if r.returncode != 0:
