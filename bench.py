@@ -108,14 +108,29 @@ class Clocks:
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
+    def wait_first(self, timeout=3.0):
+        """Block until the sampler delivered its first row (nvidia-smi start-up), so that the
+        timed region that follows is covered; returns the row count (the region's first index)."""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        self.mark = len(self.rows)
+        return self.mark
+
     def stop(self):
+        # a timed region shorter than the 100 ms sampling period may end before any sample lands in
+        # it: take the next one (the clock right at the end of the region) rather than none
+        t0 = time.time()
+        while self.proc and len(self.rows) <= getattr(self, "mark", 0) and time.time() - t0 < 0.5:
+            time.sleep(0.01)
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        rows = self.rows[getattr(self, "mark", 0):] or self.rows  # the timed region's samples
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm.sort()
@@ -369,6 +384,7 @@ def main():
     clocks = Clocks()
     clocks.start()
     time.sleep(0.3)
+    clocks.wait_first()
     launches0 = ctx.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     if dist:
