@@ -107,7 +107,8 @@ def _ipc_worker(rank, world, port, case, result_path):
     from paper_1608_08009_b200 import fks, parallel
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datetime
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
     torch.cuda.set_device(0)
     dxd, dv, M, N, bc, _, solid_at = case
     L, h, dt, F, ghosts = _problem(dxd, dv, M, N, bc, seed=dxd + world)
