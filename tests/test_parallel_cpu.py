@@ -1,5 +1,6 @@
 """Multi-rank host logic on CPU (gloo, world size 2-3): slab decomposition, face kinds, and the
 halo exchange, checked end to end against the oracle's single-domain transport gather."""
+import datetime
 import os
 import socket
 
@@ -57,7 +58,7 @@ def _global_state(case):
 def _worker(rank, world, port, case, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
     try:
         dx, dv, M, N, L, bc = CASES[case]
         n = N ** dv
@@ -115,7 +116,7 @@ def _worker_libplan(rank, world, port, case, out):
     from paper_1608_08009_b200 import fks
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
     try:
         dx, dv, M, N, L, bc = CASES[case]
         n = N ** dv
